@@ -1,0 +1,368 @@
+#!/usr/bin/env python
+"""Benchmark of the SMA hot path (arXiv 1901.02244, Alg. 1) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl sma|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1)
+
+Workload (BASELINE.json metric, config C4): one SMA round at ResNet-50 size,
+d = 25,557,032 parameters, k = 16 replicas in total (strong scaling: r = 16/N
+per GPU), alpha = 1/16, gamma = 0.1, mu = 0.9, fp32, synthetic gradients
+ resident in HBM.  A "step" is one full round
+(a3-a9: replica kernel, per-GPU partial, [NCCL RS, shard update, NCCL AG]).
+The per-round working set (>= 3.4 GB per GPU at N = 1, 0.85 GB at N = 8) is
+far larger than the 126 MB L2, so no L2 flush is needed between steps.
+
+Prints ONE JSON line on rank 0 (the driver's contract), with `roofline`
+(dominant kernel: the replica kernel, algorithmic bytes / CUDA-event time vs
+MEASURED_PEAKS.json), `cpu_baseline` (the fp64 oracle on the host, bounded
+sample), `e2e` (through the C ABI with host buffers) and `clocks`.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import sma_inputs  # noqa: E402
+
+METRIC = ("SMA rounds/sec and HBM/NVLink GB/s vs peak at ResNet-50 size, k replicas, "
+          "1/2/4/8 B200")
+UNIT = "rounds/s"
+HBM_FALLBACK_GBS = 6650.0
+NVLINK_PEAK_GBS = 770.0   # measured per-direction peer bandwidth (B200_PROFILING.md)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--impl", choices=["sma", "reference"], default="sma")
+    ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4", "C5"])
+    ap.add_argument("--k", type=int, default=None, help="override total replicas")
+    ap.add_argument("--mode", choices=["auto", "A", "B"], default="auto",
+                    help="collective path mode when N > 1 (auto = B, the overlapped round)")
+    ap.add_argument("--tma", action="store_true", help="TMA-staged replica kernel variant")
+    ap.add_argument("--matc", action="store_true", help="north_star-literal c_j materialisation")
+    ap.add_argument("--force-collective", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        try:
+            j = json.load(open(p))
+            return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except Exception:
+            pass
+    return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown",
+              "clocks_event_reasons.sw_thermal_slowdown", "clocks_event_reasons.sw_power_cap"]
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={','.join(self.FIELDS)}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_baseline(d, k, alpha, gamma, mu, n_idx=1 << 23, rounds=3):
+    """The oracle as it stands (single thread, fp64), on a bounded sample of
+    the same workload: all k replicas, `rounds` rounds, n_idx seeded parameter
+    indices (SMA with given gradients is separable per index, so the sample
+    runs the identical per-parameter computation).  Scaled to rounds/s of the
+    full d: value = rounds * (n_idx / d) / seconds."""
+    import oracle
+    oracle.build()
+    n_idx = min(n_idx, d)
+    idx = np.sort(np.random.default_rng(0).choice(d, n_idx, replace=False)) if n_idx < d \
+        else np.arange(d)
+    t = time.perf_counter()
+    oracle.run_synth(d, k, alpha, gamma, mu, rounds, sma_inputs.SEED_W, sma_inputs.SEED_G, idx,
+                     want_W=False)
+    dt = time.perf_counter() - t
+    return {"value": rounds * (n_idx / d) / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{rounds} full SMA rounds (k={k}) over {n_idx} of d={d} parameter "
+                      f"indices, fp64 single-thread C oracle, {dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = sma_inputs.CONFIGS[args.config]
+    d = cfg["d"]
+    k = args.k or 16
+    alpha, gamma, mu = float(np.float32(1 / k)), float(np.float32(0.1)), float(np.float32(0.9))
+    import oracle
+    oracle.build()
+    n_idx = min(d, 1 << 20)   # bounded sample per step (~0.3 s of CPU per step at C4)
+    rng = np.random.default_rng(1)
+    idx = np.sort(rng.choice(d, n_idx, replace=False)) if n_idx < d else np.arange(d)
+    state = oracle.State.init(sma_inputs.w0(d, idx=idx).astype(np.float64), k)
+    step_times = []
+    for s in range(args.warmup + args.steps):
+        t = time.perf_counter()
+        G = np.stack([oracle.synth_grad(d, k, s, j, sma_inputs.SEED_G, idx) for j in range(k)])
+        state.round(G, alpha, gamma, mu)
+        dt = time.perf_counter() - t
+        if s >= args.warmup:
+            step_times.append(dt)
+    tot = sum(step_times)
+    value = args.steps * (n_idx / d) / tot
+    sample = (f"each step: one full SMA round (k={k}, synthetic gradients generated in the "
+              f"step) over {n_idx} of d={d} parameter indices; fp64 single-thread C oracle")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args.config, d, k), "d": d, "k": k},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_name(cfg, d, k):
+    names = {"C2": "LeNet-sized", "C3": "ResNet-32-sized", "C4": "ResNet-50-sized",
+             "C5": "VGG-16-sized"}
+    return f"{cfg}: SMA round, {names[cfg]} vector d={d}, k={k} replicas, fp32"
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1901_02244_b200 import sma
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    cfg = sma_inputs.CONFIGS[args.config]
+    d = cfg["d"]
+    k = args.k or 16
+    alpha, gamma, mu = float(np.float32(1 / k)), float(np.float32(0.1)), float(np.float32(0.9))
+
+    collective = world > 1 or args.force_collective
+    mode = "fused" if not collective else ("A" if args.mode == "A" else "B")
+    flags = sma.FLAG_TIMING
+    if collective:
+        flags |= sma.FLAG_FORCE_COLLECTIVE
+        if mode == "B":
+            flags |= sma.FLAG_OVERLAP
+    if args.tma:
+        flags |= sma.FLAG_KERNEL_TMA
+    if args.matc:
+        flags |= sma.FLAG_MATERIALIZE_C
+
+    nccl_id = None
+    if world > 1:
+        obj = [sma.sma_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+
+    w0 = sma_inputs.w0(d)
+    h = sma.Sma(d, k, alpha, gamma, mu, w0, rank=rank, world=world, device=local,
+                nccl_id=nccl_id, flags=flags)
+    r = h.local_count
+    stream = torch.cuda.Stream()
+    h.synth_grads(0, sma_inputs.SEED_G, stream)   # inputs resident in HBM before timing
+    stream.synchronize()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- warm-up
+    for _ in range(args.warmup):
+        h.step(stream)
+    barrier()
+    h.kernel_time(reset=True)
+
+    # ------------------------------------------------------------ timed region
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    l0 = h.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        h.step(stream)
+    ev1.record(stream)
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = h.launch_count() - l0
+    clk = clocks.stop()
+    kern_ms, kern_n = h.kernel_time(reset=True)
+
+    t = torch.tensor([ms, kern_ms / max(kern_n, 1), float(launches)], dtype=torch.float64,
+                     device="cuda")
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t.clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms_max, kern_avg = float(tmax[0]), float(tmax[1])
+        launches_total = int(tsum[2])
+    else:
+        ms_max, kern_avg, launches_total = ms, kern_ms / max(kern_n, 1), launches
+
+    # ------------------------------------------------------------------ e2e
+    e2e = None
+    if not args.no_e2e:
+        pinned = [torch.empty(d, dtype=torch.float32).pin_memory() for _ in range(r)]
+        for s_ in range(r):
+            pinned[s_].copy_(torch.from_numpy(sma_inputs.grad(0, h.local_first + s_, k, d)))
+        zout = torch.empty(d, dtype=torch.float32).pin_memory()
+
+        def e2e_step():
+            for s_ in range(r):
+                sma.sma_set_learner_grads_host(h.h, h.local_first + s_, pinned[s_], stream)
+            h.step(stream)
+            sma.sma_get_central(h.h, zout, False)
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        barrier()
+        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+        e2e = {"value": args.e2e_steps / float(e2e_s[0]), "unit": UNIT,
+               "h2d_bytes_per_step": 4 * d * k, "d2h_bytes_per_step": 4 * d * world,
+               "how": "per step: sma_set_learner_grads_host (pinned host -> device) for every "
+                      "local learner, sma_step, sma_get_central (device -> host); wall clock, "
+                      "max over ranks"}
+
+    if rank == 0:
+        d_pad = h.d_pad
+        peak, peak_src = measured_peaks()
+        if mode == "fused":
+            alg_bytes = 4 * d_pad * (3 * r + 3)
+            kname = "replica_step_ldg<kFused>"
+        else:
+            alg_bytes = 4 * d_pad * (3 * r + 2)
+            kname = "replica_step_ldg<kPartial%s>" % mode
+        if args.matc:
+            alg_bytes = 4 * d_pad * (6 * r + (3 if mode == "fused" else 2))
+        achieved = alg_bytes / (kern_avg * 1e-3) / 1e9
+        traffic = None
+        tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_n{world}_{mode}.json")
+        if os.path.exists(tpath):
+            try:
+                traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        value = args.steps / (ms_max * 1e-3)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_name(args.config, d, k), "d": d, "d_pad": d_pad,
+                       "k": k, "replicas_per_gpu": r, "alpha": alpha, "gamma": gamma, "mu": mu,
+                       "mode": mode, "kernel": "tma" if args.tma else "ldg",
+                       "materialize_c": bool(args.matc),
+                       "parallelism": f"sma-dp{world}" + ("" if world == 1 else "+nccl-rs/ag"),
+                       "l2": "no flush: per-round working set "
+                             f"{(alg_bytes / 1e9):.2f} GB/GPU >> 126 MB L2"},
+            "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_avg,
+                         "peak_source": peak_src, "vs_8TBs_spec": achieved / 8000.0},
+            "gpu_launches": launches_total,
+            "clocks": clk,
+        }
+        if world > 1:
+            link = 2 * 4 * d_pad * (world - 1) / world
+            line["nvlink"] = {"link_bytes_per_gpu_per_round": link,
+                              "note": "RS+AG bytes per GPU per round (nccl-tests bus "
+                                      "convention); overlapped with the replica kernel in Mode B",
+                              "bus_gbs_if_serial": link / (ms_max / args.steps * 1e-3) / 1e9,
+                              "peak_gbs": NVLINK_PEAK_GBS}
+        if e2e:
+            line["e2e"] = e2e
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(d, k, alpha, gamma, mu)
+        print(json.dumps(line), flush=True)
+    h.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,275 @@
+/*
+ * sma.h -- C ABI of libsma, the B200-native hot path of Synchronous Model
+ * Averaging (SMA), Algorithm 1 of Koliousis et al., "Crossbow: Scaling Deep
+ * Learning with Small Batch Sizes on Multi-GPU Servers", arXiv 1901.02244.
+ * Citations "P:n" are lines of the paper text; "S:n" lines of
+ * SPEC.md; "Rn" the readings listed in DESIGN.md.
+ *
+ * One round (sma_step) is one iteration of Alg. 1 over all k
+ * learners:   c_j = alpha (w_j - z);   w_j <- w_j - gamma g_j - c_j;
+ *             z <- z + sum_j c_j + mu (z - z_prev);   z_prev <- old z.
+ *
+ * Conventions for every entry point
+ *   - Scalars are fp32, vectors fp32, contiguous, unit stride.  d is the model
+ *     size (number of parameters).  Parameter p of replica j is
+ *     element p of that replica's vector.
+ *   - Ownership: the handle owns every device buffer, stream, event, graph and
+ *     NCCL communicator it creates.  Inputs marked BORROWED must stay valid
+ *     (and unmodified) as stated; everything else is copied.  Outputs go to
+ *     caller-owned memory.
+ *   - Errors: every call returns sma_status; no C++ exception crosses the ABI.
+ *     Arguments are validated before anything is enqueued, so a call that
+ *     returns SMA_ERR_INVALID_ARG / _NOT_LOCAL / _GRADS_MISSING / _STATE has
+ *     changed nothing.  sma_last_error() returns a thread-local message for
+ *     the most recent failure on the calling thread.
+ *   - Threading: one issuing host thread per handle.  sma_create,
+ *     sma_step and sma_destroy are COLLECTIVE when world > 1: every rank calls
+ *     them in the same order with identical (d, k, alpha, gamma, mu, flags).
+ *   - Streams: calls taking `cuda_stream` (a cudaStream_t, NULL = legacy
+ *     default stream) enqueue their work after all prior work on that stream,
+ *     and later work on that stream is ordered after them.  No call in the
+ *     hot path synchronises the host.
+ *   - There is no CPU fallback: every arithmetic step runs in this library's
+ *     CUDA kernels (and NCCL for the inter-GPU exchange).  Without a usable
+ *     sm_100 device, sma_create fails with SMA_ERR_CUDA.
+ */
+#ifndef SMA_H_
+#define SMA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SMA_ABI_VERSION 1
+#define SMA_MAX_LOCAL_REPLICAS 64   /* r = replicas per GPU, P:1193-1194 ("m") */
+#define SMA_NCCL_ID_BYTES 128
+
+typedef struct sma_handle sma_handle;   /* opaque; owns all device state */
+
+typedef enum {
+    SMA_OK = 0,
+    SMA_ERR_INVALID_ARG = 1,   /* bad size/index/pointer/alignment/hyper-parameter */
+    SMA_ERR_NOT_LOCAL = 2,     /* replica j lives on another rank */
+    SMA_ERR_GRADS_MISSING = 3, /* a local learner has no gradient registered */
+    SMA_ERR_NONFINITE = 4,     /* a NaN/Inf appeared (only with SMA_FLAG_CHECK_FINITE) */
+    SMA_ERR_CUDA = 5,          /* CUDA runtime error (message in sma_last_error) */
+    SMA_ERR_NCCL = 6,          /* NCCL error or NCCL library not loadable */
+    SMA_ERR_OOM = 7,           /* device allocation failed */
+    SMA_ERR_STATE = 8          /* call not valid in the handle's current state */
+} sma_status;
+
+/* Flags (sma_config.flags). */
+enum {
+    /* Mode B (lookahead): the inter-GPU z-sync of round i
+     * runs on a second stream concurrently with the replica kernel of round i,
+     * using the identity z^{i+1} = z^i + alpha Q^i + (mu - alpha k)(z^i - z^{i-1}),
+     * Q^i = sum_j (w_j^i - z^{i-1}).  Exact in exact arithmetic; implements the
+     * paper's overlap of global synchronisation with the next learning tasks
+     * (P:885-889).  Only meaningful on the collective path. */
+    SMA_FLAG_OVERLAP = 1u,
+    /* North_star-literal variant: the replica kernel writes every c_j to HBM
+     * and a separate warp-shuffle/block-tree kernel reduces them.
+     * Moves 4 d_pad (6r+1) bytes per round instead of 4 d_pad (3r+2). */
+    SMA_FLAG_MATERIALIZE_C = 2u,
+    /* Record a device flag when any updated value is not finite; sma_step then
+     * returns SMA_ERR_NONFINITE at the NEXT call that synchronises
+     * (sma_get_central / sma_get_replica / sma_check_finite). */
+    SMA_FLAG_CHECK_FINITE = 4u,
+    /* Capture the round into a CUDA graph on first use and replay it; the
+     * graph is re-instantiated when registered gradient pointers change. */
+    SMA_FLAG_CUDA_GRAPH = 8u,
+    /* Use the n>1 structure (replica partial -> NCCL reduce-scatter -> shard
+     * update -> NCCL all-gather) even when world == 1 (a 1-rank NCCL
+     * communicator).  Exercises the multi-GPU path on one GPU. */
+    SMA_FLAG_FORCE_COLLECTIVE = 16u,
+    /* Time every replica-kernel launch with CUDA events on its own stream
+     * (sma_kernel_time). */
+    SMA_FLAG_TIMING = 32u,
+    /* Replica kernel variant: TMA bulk-copy (cp.async.bulk) shared-memory
+     * staging with an mbarrier pipeline instead of direct 128-bit loads. */
+    SMA_FLAG_KERNEL_TMA = 64u
+};
+
+typedef struct {
+    int64_t  d;          /* model size, >= 1 */
+    int32_t  k;          /* total learners = replicas, >= 1     */
+    float    alpha;      /* correction weight, finite; paper: ~1/k             (R5) */
+    float    gamma;      /* learning rate, finite; multiplies RAW gradients    (R1) */
+    float    mu;         /* central-model momentum, finite */
+    int32_t  rank;       /* this process's rank in [0, world)                               */
+    int32_t  world;      /* number of GPUs n, >= 1; replicas are block-split over ranks      */
+    int32_t  device;     /* CUDA device ordinal used by this rank                           */
+    const void* nccl_id; /* SMA_NCCL_ID_BYTES from sma_nccl_unique_id() on rank 0, the same
+                            bytes on every rank; required iff world > 1 (copied)            */
+    uint32_t flags;      /* SMA_FLAG_* */
+} sma_config;
+
+/* ---------------------------------------------------------------- lifecycle */
+
+/* Create the state of Alg. 1 lines 1-2 on this rank:
+ *   z <- w0;  z_prev <- w0 (R2: the paper's "empty" read as zero momentum in
+ *   round 1);  w_j <- w0 for every local replica j (R3; "initialised with the
+ *   latest value of the average model").
+ * w0_host: d floats in host memory (copied; need not be pinned).
+ * Device layout (one allocation per array): W [r][d_pad],
+ * z [2][d_pad] (ping-pong: the current z and z_prev), plus P [d_pad],
+ * S [d_pad/n] and, with SMA_FLAG_OVERLAP, Q [2][d_pad] on the collective
+ * path.  d_pad = sma_plan_d_pad(d, world); the padding [d, d_pad) is 0 and
+ * stays exactly 0.  COLLECTIVE when world > 1 (ncclCommInitRank).
+ * Errors: INVALID_ARG (d < 1, k < 1, world < 1, rank out of range, more than
+ * SMA_MAX_LOCAL_REPLICAS replicas on this rank, non-finite hyper-parameter,
+ * missing nccl_id when world > 1, NULL pointers), CUDA, NCCL, OOM.
+ * On failure *out is set to NULL and nothing is leaked. */
+sma_status sma_create(const sma_config* cfg, const float* w0_host, sma_handle** out);
+
+/* Free everything the handle owns (after finishing its enqueued work).
+ * NULL is a no-op.  COLLECTIVE when world > 1. */
+void sma_destroy(sma_handle* h);
+
+/* --------------------------------------------------------- gradient intake */
+
+/* Register the RAW gradient of learner j (grad l_{B_j}(w_j), Alg. 1 line 8,
+ * P:577; gamma is applied by sma_step, R1) as a device pointer.
+ * j: GLOBAL learner index in [0, k); must live on this rank.
+ * g_dev: d floats on this rank's device, 16-byte aligned.  BORROWED: must stay
+ * valid and unmodified until the next sma_step that reads it has completed on
+ * the device; the registration persists across steps until replaced.
+ * Errors: INVALID_ARG (j out of range, NULL or misaligned pointer), NOT_LOCAL. */
+sma_status sma_set_learner_grads(sma_handle* h, int32_t j, const float* g_dev);
+
+/* Copy a RAW gradient from host memory into the handle's own gradient buffer
+ * for learner j and register it (replaces any device registration of j).
+ * g_host: d floats (pinned memory makes the copy asynchronous; pageable
+ * memory works but the copy is then staged by the driver).  The copy is
+ * enqueued on cuda_stream; g_host must stay valid until it has completed.
+ * Errors: INVALID_ARG, NOT_LOCAL, CUDA, OOM. */
+sma_status sma_set_learner_grads_host(sma_handle* h, int32_t j, const float* g_host,
+                                      void* cuda_stream);
+
+/* Fill the handle's gradient buffers of all LOCAL learners with the synthetic
+ * raw gradients of round `round` (R9):
+ *   g_j^i[p] = (U(seed, (i k + j) d + p) - 1/2) 2^-4,
+ *   U(s, c) = (splitmix64(splitmix64(s) + c) >> 40) 2^-24,
+ * and register them.  Enqueued on cuda_stream.  Errors: CUDA, OOM. */
+sma_status sma_synth_grads(sma_handle* h, int64_t round, uint64_t seed, void* cuda_stream);
+
+/* ------------------------------------------------------------------- round */
+
+/* One iteration of Alg. 1 for all k learners:
+ *   a3 c_j = alpha (w_j - z) against the same z for all j   (line 9)
+ *   a4 w_j <- w_j - gamma g_j - c_j, in place               (line 10)
+ *   a5 per-GPU partial of sum_j c_j
+ *   a6 NCCL reduce-scatter of the partials (world > 1)
+ *   a7 z <- z + sum c + mu (z - z_prev) on this GPU's shard (line 13)
+ *   a8 NCCL all-gather of z (world > 1)
+ *   z_prev <- old z is a buffer swap (line 14).
+ * world == 1 without FORCE_COLLECTIVE: a3-a7 are ONE fused kernel.
+ * Every local learner must have a registered gradient (else GRADS_MISSING).
+ * COLLECTIVE when world > 1.  Errors: GRADS_MISSING, CUDA, NCCL. */
+sma_status sma_step(sma_handle* h, void* cuda_stream);
+
+/* ----------------------------------------------------------------- outputs */
+
+/* Copy the central model z (Alg. 1 output) into z_out (d floats;
+ * device memory of this rank's GPU if out_is_device, else host memory).
+ * Synchronises the host with all work the handle has enqueued.  Every rank
+ * holds the full z.  Errors: INVALID_ARG, CUDA, NONFINITE (CHECK_FINITE). */
+sma_status sma_get_central(sma_handle* h, float* z_out, int out_is_device);
+
+/* Same for z_prev (the central model at the beginning of the previous round,
+ * P:630-631), needed to checkpoint/resume without losing momentum. */
+sma_status sma_get_central_prev(sma_handle* h, float* out, int out_is_device);
+
+/* Copy local replica j (global index) into out (d floats). Synchronises. */
+sma_status sma_get_replica(sma_handle* h, int32_t j, float* out, int out_is_device);
+
+/* Overwrite local replica j / the central model / z_prev with d floats
+ * (checkpoint restore, distinct initial replicas for tests, R3).
+ * Synchronises.  Errors: INVALID_ARG, NOT_LOCAL, CUDA. */
+sma_status sma_set_replica(sma_handle* h, int32_t j, const float* w, int in_is_device);
+sma_status sma_set_central(sma_handle* h, const float* z, const float* z_prev, int in_is_device);
+
+/* Read-only device views (valid until the next sma_step / sma_destroy):
+ * replica j's d_pad floats, and the current z (d_pad floats). */
+sma_status sma_replica_device_ptr(sma_handle* h, int32_t j, const float** w_dev);
+sma_status sma_central_device_ptr(sma_handle* h, const float** z_dev);
+
+/* SMA restart: every local replica := z and
+ * z_prev := z (zero momentum).  Enqueued on cuda_stream. */
+sma_status sma_restart(sma_handle* h, void* cuda_stream);
+
+/* Change alpha, gamma, mu between rounds (online adaptation).
+ * Errors: INVALID_ARG (non-finite). */
+sma_status sma_set_hparams(sma_handle* h, float alpha, float gamma, float mu);
+
+/* If SMA_FLAG_CHECK_FINITE: synchronise and report whether any non-finite
+ * value has been produced so far (*flag = 1) ; clears the flag. */
+sma_status sma_check_finite(sma_handle* h, int* flag);
+
+/* --------------------------------------------------- built-in learner (a2') */
+
+/* Attach the built-in learner (kind 0 = softmax regression):
+ * params layout W [classes][in_dim] row-major then b [classes] (R12), so
+ * d must equal classes*in_dim + classes.  X_dev: n_samples x in_dim fp32
+ * row-major, y_dev: n_samples int32 labels in [0, classes); both on this
+ * rank's device and BORROWED for the handle's lifetime.  batch = b rows per
+ * learner per round; batch_seed keys the per-epoch permutation (R10).
+ * Errors: INVALID_ARG (kind, sizes, n_samples < k*batch). */
+sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32_t hidden,
+                              int32_t classes, int32_t batch, const float* X_dev,
+                              const int32_t* y_dev, int64_t n_samples, uint64_t batch_seed);
+
+/* For every local learner j: gather batch B(round, j) (R10), compute the
+ * batch-mean gradient (Eq. 2) of the mean cross-entropy at the
+ * current replica w_j (max-subtracted softmax, R16) in fp32 FFMA (no TF32),
+ * into the handle's gradient buffer, and register it.  Enqueued on
+ * cuda_stream.  Errors: STATE (no learner attached), CUDA. */
+sma_status sma_learner_grads(sma_handle* h, int64_t round, void* cuda_stream);
+
+/* ------------------------------------------------ bookkeeping (host only) */
+/* Pure functions of their arguments; no device, no handle (bit-exact with
+ * the oracle's independent implementation). */
+
+/* d_pad = roundup(d, lcm(512, 64 n)); every shard is d_pad/n floats. */
+int64_t sma_plan_d_pad(int64_t d, int32_t world);
+/* Replica j -> (rank, slot): rank g with floor(g k/n) <= j < floor((g+1) k/n). */
+sma_status sma_plan_replica_location(int32_t k, int32_t world, int32_t j,
+                                     int32_t* rank, int32_t* slot);
+/* First global replica index and count r on `rank`. */
+sma_status sma_plan_local_replicas(int32_t k, int32_t world, int32_t rank,
+                                   int32_t* first, int32_t* count);
+/* Shard of rank g: [offset, offset + length) of the padded vector. */
+sma_status sma_plan_shard_range(int64_t d, int32_t world, int32_t rank,
+                                int64_t* offset, int64_t* length);
+/* Batch of learner j in round i (R10): b row indices into [0, N). */
+sma_status sma_plan_batch_indices(int64_t n_samples, int32_t k, int32_t batch,
+                                  uint64_t batch_seed, int64_t round, int32_t j,
+                                  int64_t* out);
+
+/* ------------------------------------------------------------- utilities */
+
+/* Write a fresh NCCL unique id (SMA_NCCL_ID_BYTES) to out (rank 0 only;
+ * broadcast the bytes to the other ranks).  Errors: NCCL. */
+sma_status sma_nccl_unique_id(void* out);
+
+/* With SMA_FLAG_TIMING: total device milliseconds and number of replica-
+ * kernel launches measured since the last reset (synchronises). */
+sma_status sma_kernel_time(sma_handle* h, double* total_ms, int64_t* launches, int reset);
+
+/* Number of libsma CUDA kernels this handle has launched (NCCL collectives not counted). */
+int64_t sma_launch_count(const sma_handle* h);
+
+/* Shape of this rank's state. */
+sma_status sma_info(const sma_handle* h, int64_t* d_pad, int32_t* local_first,
+                    int32_t* local_count, int64_t* shard_offset, int64_t* shard_length);
+
+const char* sma_last_error(void);
+int sma_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SMA_H_ */

@@ -1,0 +1,66 @@
+// sma_internal.h -- declarations shared by libsma's runtime (sma_runtime.cu) and
+// its kernels (sma_kernels.cu).  Not part of the ABI (include/sma.h is).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sma.h"
+
+namespace sma {
+
+// Up to SMA_MAX_LOCAL_REPLICAS gradient pointers, passed BY VALUE as a kernel
+// parameter (constant bank: broadcast to every thread, no extra global load,
+// and baked into a captured CUDA graph together with the other arguments).
+struct GradTable {
+  const float* p[SMA_MAX_LOCAL_REPLICAS];
+};
+
+// What the replica kernel emits besides the updated replicas.
+enum ReplicaMode : int {
+  kFused = 0,    // n == 1: also z_next = z + sum c + mu (z - z_prev)   (Alg. 1 line 13)
+  kPartialA = 1, // collective path, paper order: P = sum_{local j} c_j
+  kPartialB = 2, // collective path, lookahead: Q = sum_{local j} (w_j' - z)
+};
+
+struct ReplicaArgs {
+  float* W;            // [r][ld] replicas, updated in place
+  int64_t ld;          // row stride in floats (= d_pad, multiple of 512)
+  int r;               // local replica count
+  GradTable g;         // raw gradients, d floats each (16-byte aligned)
+  int64_t d;           // valid length (g is read only below d)
+  int64_t n4;          // d_pad / 4  (float4 chunks)
+  const float* z;      // current central model z^i            [d_pad]
+  float* zprev_next;   // kFused: reads z^{i-1}, writes z^{i+1} in place [d_pad]
+  float* out;          // kPartialA: P, kPartialB: Q          [d_pad]
+  float* C;            // MATERIALIZE_C: c_j buffer [r][ld] (else nullptr)
+  float alpha, gamma, mu;
+  int* nonfinite;      // CHECK_FINITE flag or nullptr
+};
+
+// Launchers (return the launch error, never synchronise).
+cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a, int num_sms,
+                                cudaStream_t s);
+// MATERIALIZE_C second pass: reduce C over replicas (warp shuffle + block tree),
+// then the fused z update (mode kFused) or the partial (kPartialA).
+cudaError_t launch_reduce_corrections(int mode, const ReplicaArgs& a, int num_sms,
+                                      cudaStream_t s);
+// Shard update after the reduce-scatter (a7).  Mode A: z' = z + S + mu (z - zp);
+// Mode B: z' = z + alpha S + (mu - alpha k)(z - zp).  zprev_next is in/out.
+cudaError_t launch_zsync(int mode, const float* S, const float* z, float* zprev_next,
+                         int64_t n4, float alpha, float mu, float coef_b, int* nonfinite,
+                         int num_sms, cudaStream_t s);
+// Mode B prologue: Q = sum_j (w_j - zprev) over local replicas.
+cudaError_t launch_q_prologue(const float* W, int64_t ld, int r, const float* zprev, float* Q,
+                              int64_t n4, int num_sms, cudaStream_t s);
+// Synthetic raw gradients of round `round` for local replicas [j0, j0 + r).
+cudaError_t launch_synth_grads(float* G, int64_t ld, int r, int j0, int k, int64_t d,
+                               int64_t round, uint64_t seed, int num_sms, cudaStream_t s);
+// Softmax-regression learner gradient for the r local replicas.
+cudaError_t launch_softmax_grad(const float* X, const int32_t* y, const int32_t* perm,
+                                int64_t pos0, int b, int in_dim, int classes, const float* W,
+                                int64_t ld, int r, int j0, float* G, cudaStream_t s);
+// Broadcast: dst rows [r][ld] := src [ld]   and   y := x   (restart / init).
+cudaError_t launch_broadcast_rows(float* dst, int64_t ld, int r, const float* src, int64_t n4,
+                                  int num_sms, cudaStream_t s);
+
+}  // namespace sma

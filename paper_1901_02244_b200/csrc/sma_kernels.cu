@@ -1,0 +1,503 @@
+// sma_kernels.cu -- sm_100a kernels of the SMA hot path (arXiv 1901.02244, Alg. 1).
+//
+// All kernels are HBM-bandwidth-bound streaming kernels (about 5 flop per 12
+// bytes), so they are written for the memory system, not the tensor cores:
+// 128-bit coalesced accesses, L1 bypass for single-use streams, a persistent
+// grid of (#SMs x resident CTAs), and several independent 16-byte loads in
+// flight per thread.  Each floating-point operation is written with an
+// explicit-rounding intrinsic so the fp32 operation sequence is fixed (and
+// documented in DESIGN.md "Arithmetic") rather than left to FMA contraction.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sma_internal.h"
+
+namespace sma {
+namespace {
+
+// ---------------------------------------------------------------- memory ops
+// Single-use streams: do not allocate in L1.  `.nc` only for data that is
+// read-only for the whole kernel (gradients, z); replicas are read then
+// written by the same thread, so they use the coherent path.
+__device__ __forceinline__ float4 ld_ro(const float* p) {
+  float4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ float4 ld_rw(const float* p) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st4(float* p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};"
+               :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+// Gradient chunk that straddles (or lies beyond) d: scalar loads, zeros past d.
+__device__ __forceinline__ float4 ld_tail(const float* g, int64_t p0, int64_t d) {
+  float4 v;
+  v.x = (p0 + 0 < d) ? g[p0 + 0] : 0.f;
+  v.y = (p0 + 1 < d) ? g[p0 + 1] : 0.f;
+  v.z = (p0 + 2 < d) ? g[p0 + 2] : 0.f;
+  v.w = (p0 + 3 < d) ? g[p0 + 3] : 0.f;
+  return v;
+}
+
+__device__ __forceinline__ bool finite4(float4 v) {
+  return isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w);
+}
+
+// ------------------------------------------------------------- arithmetic
+// Alg. 1 line 9:  c = alpha (w - z)
+// Alg. 1 line 10: w' = (w - gamma g) - c        (w - gamma g rounded once, FMA)
+struct StepOut { float wn, c; };
+__device__ __forceinline__ StepOut sma_elem(float w, float g, float z, float alpha, float gamma) {
+  const float c = __fmul_rn(alpha, __fsub_rn(w, z));
+  const float wn = __fsub_rn(__fmaf_rn(-gamma, g, w), c);
+  return {wn, c};
+}
+// Alg. 1 line 13: z' = (z + sum c) + mu (z - z_prev)
+__device__ __forceinline__ float central_elem(float z, float csum, float zp, float mu) {
+  return __fadd_rn(__fadd_rn(z, csum), __fmul_rn(mu, __fsub_rn(z, zp)));
+}
+
+template <int MODE>
+__device__ __forceinline__ void replica_update4(float4& w, const float4 g, const float4 z,
+                                               float4& acc, float4& c4, float alpha, float gamma) {
+  StepOut o;
+  o = sma_elem(w.x, g.x, z.x, alpha, gamma); w.x = o.wn; c4.x = o.c;
+  o = sma_elem(w.y, g.y, z.y, alpha, gamma); w.y = o.wn; c4.y = o.c;
+  o = sma_elem(w.z, g.z, z.z, alpha, gamma); w.z = o.wn; c4.z = o.c;
+  o = sma_elem(w.w, g.w, z.w, alpha, gamma); w.w = o.wn; c4.w = o.c;
+  if (MODE == kPartialB) {  // Q accumulates (w' - z), DESIGN.md "Mode B"
+    acc.x = __fadd_rn(acc.x, __fsub_rn(w.x, z.x));
+    acc.y = __fadd_rn(acc.y, __fsub_rn(w.y, z.y));
+    acc.z = __fadd_rn(acc.z, __fsub_rn(w.z, z.z));
+    acc.w = __fadd_rn(acc.w, __fsub_rn(w.w, z.w));
+  } else {                  // sum_j c_j in ascending local j (R7)
+    acc.x = __fadd_rn(acc.x, c4.x);
+    acc.y = __fadd_rn(acc.y, c4.y);
+    acc.z = __fadd_rn(acc.z, c4.z);
+    acc.w = __fadd_rn(acc.w, c4.w);
+  }
+}
+
+// ------------------------------------------------------- replica kernel (LDG)
+// One thread owns one float4 column chunk of the padded vector per iteration
+// and walks the r local replicas in groups of UJ, issuing the UJ replica and
+// UJ gradient loads of a group before any arithmetic (2*UJ independent
+// 16-byte loads in flight per thread).  The cross-replica sum is a register
+// accumulation: every replica of a column is owned by the same thread, so no
+// shuffle or shared memory is needed for it.
+constexpr int kThreads = 256;
+constexpr int kUJ = 4;
+
+// Finish one float4 column chunk: the fused central update (n == 1) or the
+// per-GPU partial (collective path).
+template <int MODE>
+__device__ __forceinline__ void replica_finish(const ReplicaArgs& a, int64_t p0, const float4 z,
+                                               const float4 acc, bool& bad) {
+  if (MODE == kFused) {
+    const float4 zp = ld_rw(a.zprev_next + p0);
+    float4 zn;
+    zn.x = central_elem(z.x, acc.x, zp.x, a.mu);
+    zn.y = central_elem(z.y, acc.y, zp.y, a.mu);
+    zn.z = central_elem(z.z, acc.z, zp.z, a.mu);
+    zn.w = central_elem(z.w, acc.w, zp.w, a.mu);
+    st4(a.zprev_next + p0, zn);
+    bad |= !finite4(zn);
+  } else {
+    st4(a.out + p0, acc);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreads, 4) replica_step_ldg(const ReplicaArgs a) {
+  const int64_t stride = (int64_t)gridDim.x * kThreads;
+  const int64_t dfull4 = a.d >> 2;  // chunks entirely below d: vector path
+  const bool matc = a.C != nullptr;
+  bool bad = false;
+  for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < dfull4; c += stride) {
+    const int64_t p0 = c << 2;
+    const float4 z = ld_ro(a.z + p0);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 c4;
+    int j = 0;
+    for (; j + kUJ <= a.r; j += kUJ) {
+      float4 w[kUJ], g[kUJ];
+#pragma unroll
+      for (int u = 0; u < kUJ; ++u) w[u] = ld_rw(a.W + (int64_t)(j + u) * a.ld + p0);
+#pragma unroll
+      for (int u = 0; u < kUJ; ++u) g[u] = ld_ro(a.g.p[j + u] + p0);
+#pragma unroll
+      for (int u = 0; u < kUJ; ++u) {
+        replica_update4<MODE>(w[u], g[u], z, acc, c4, a.alpha, a.gamma);
+        st4(a.W + (int64_t)(j + u) * a.ld + p0, w[u]);
+        if (matc) st4(a.C + (int64_t)(j + u) * a.ld + p0, c4);
+        bad |= !finite4(w[u]);
+      }
+    }
+    for (; j < a.r; ++j) {
+      float4 w = ld_rw(a.W + (int64_t)j * a.ld + p0);
+      const float4 g = ld_ro(a.g.p[j] + p0);
+      replica_update4<MODE>(w, g, z, acc, c4, a.alpha, a.gamma);
+      st4(a.W + (int64_t)j * a.ld + p0, w);
+      if (matc) st4(a.C + (int64_t)j * a.ld + p0, c4);
+      bad |= !finite4(w);
+    }
+    if (!matc) replica_finish<MODE>(a, p0, z, acc, bad);
+  }
+  // The chunk straddling d and the zero padding [d, d_pad): gradients are read
+  // with scalar loads below d and taken as 0 above it (padding stays 0).
+  for (int64_t c = dfull4 + (int64_t)blockIdx.x * kThreads + threadIdx.x; c < a.n4; c += stride) {
+    const int64_t p0 = c << 2;
+    const float4 z = ld_ro(a.z + p0);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 c4;
+    for (int j = 0; j < a.r; ++j) {
+      float4 w = ld_rw(a.W + (int64_t)j * a.ld + p0);
+      const float4 g = ld_tail(a.g.p[j], p0, a.d);
+      replica_update4<MODE>(w, g, z, acc, c4, a.alpha, a.gamma);
+      st4(a.W + (int64_t)j * a.ld + p0, w);
+      if (matc) st4(a.C + (int64_t)j * a.ld + p0, c4);
+      bad |= !finite4(w);
+    }
+    if (!matc) replica_finish<MODE>(a, p0, z, acc, bad);
+  }
+  if (a.nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0)
+    atomicOr(a.nonfinite, 1);
+}
+
+// ---------------------------------------- MATERIALIZE_C: reduce c_j over j
+// The north_star-literal intra-GPU reduction: a warp covers 8 float4 columns
+// x 4 replica groups (lane = group*8 + column); each lane sums its replicas
+// j = group + 4*warp + 32*t, the 4 groups are combined with two xor-shuffles,
+// and the 8 warps of the block with a shared-memory tree.
+constexpr int kRedWarps = 8;
+template <int MODE>
+__global__ void __launch_bounds__(kRedWarps * 32) reduce_corrections(const ReplicaArgs a) {
+  __shared__ float4 part[kRedWarps][8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int col = lane & 7, grp = lane >> 3;
+  const int64_t ntiles = (a.n4 + 7) / 8;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t c = t * 8 + col;
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (c < a.n4) {
+      for (int j = grp + 4 * warp; j < a.r; j += 4 * kRedWarps) {
+        const float4 v = ld_ro(a.C + (int64_t)j * a.ld + (c << 2));
+        s.x = __fadd_rn(s.x, v.x); s.y = __fadd_rn(s.y, v.y);
+        s.z = __fadd_rn(s.z, v.z); s.w = __fadd_rn(s.w, v.w);
+      }
+    }
+#pragma unroll
+    for (int off = 8; off <= 16; off <<= 1) {
+      s.x = __fadd_rn(s.x, __shfl_xor_sync(0xffffffffu, s.x, off));
+      s.y = __fadd_rn(s.y, __shfl_xor_sync(0xffffffffu, s.y, off));
+      s.z = __fadd_rn(s.z, __shfl_xor_sync(0xffffffffu, s.z, off));
+      s.w = __fadd_rn(s.w, __shfl_xor_sync(0xffffffffu, s.w, off));
+    }
+    if (grp == 0) part[warp][col] = s;
+    __syncthreads();
+#pragma unroll
+    for (int h = kRedWarps / 2; h >= 1; h >>= 1) {  // block-level tree over warps
+      if (warp < h && grp == 0) {
+        float4 o = part[warp + h][col], m = part[warp][col];
+        m.x = __fadd_rn(m.x, o.x); m.y = __fadd_rn(m.y, o.y);
+        m.z = __fadd_rn(m.z, o.z); m.w = __fadd_rn(m.w, o.w);
+        part[warp][col] = m;
+      }
+      __syncthreads();
+    }
+    if (warp == 0 && grp == 0 && c < a.n4) {
+      const int64_t p0 = c << 2;
+      const float4 acc = part[0][col];
+      if (MODE == kFused) {
+        const float4 z = ld_ro(a.z + p0);
+        const float4 zp = ld_rw(a.zprev_next + p0);
+        float4 zn;
+        zn.x = central_elem(z.x, acc.x, zp.x, a.mu);
+        zn.y = central_elem(z.y, acc.y, zp.y, a.mu);
+        zn.z = central_elem(z.z, acc.z, zp.z, a.mu);
+        zn.w = central_elem(z.w, acc.w, zp.w, a.mu);
+        st4(a.zprev_next + p0, zn);
+        if (a.nonfinite && !finite4(zn)) atomicOr(a.nonfinite, 1);
+      } else {
+        st4(a.out + p0, acc);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------ shard update
+// a7 on this GPU's shard, in place into the z_prev half of the ping-pong.
+template <int MODE>
+__global__ void __launch_bounds__(kThreads) zsync_kernel(const float* __restrict__ S,
+                                                         const float* __restrict__ z,
+                                                         float* zprev_next, int64_t n4,
+                                                         float alpha, float mu, float coef_b,
+                                                         int* nonfinite) {
+  bool bad = false;
+  for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < n4;
+       c += (int64_t)gridDim.x * kThreads) {
+    const int64_t p0 = c << 2;
+    const float4 s = ld_ro(S + p0), zc = ld_ro(z + p0), zp = ld_rw(zprev_next + p0);
+    float4 zn;
+    if (MODE == kPartialA) {  // z' = z + S + mu (z - z_prev), S = sum_j c_j
+      zn.x = central_elem(zc.x, s.x, zp.x, mu);
+      zn.y = central_elem(zc.y, s.y, zp.y, mu);
+      zn.z = central_elem(zc.z, s.z, zp.z, mu);
+      zn.w = central_elem(zc.w, s.w, zp.w, mu);
+    } else {  // z' = (z + alpha S) + (mu - alpha k)(z - z_prev), S = sum_j (w_j - z_prev)
+      zn.x = __fadd_rn(__fmaf_rn(alpha, s.x, zc.x), __fmul_rn(coef_b, __fsub_rn(zc.x, zp.x)));
+      zn.y = __fadd_rn(__fmaf_rn(alpha, s.y, zc.y), __fmul_rn(coef_b, __fsub_rn(zc.y, zp.y)));
+      zn.z = __fadd_rn(__fmaf_rn(alpha, s.z, zc.z), __fmul_rn(coef_b, __fsub_rn(zc.z, zp.z)));
+      zn.w = __fadd_rn(__fmaf_rn(alpha, s.w, zc.w), __fmul_rn(coef_b, __fsub_rn(zc.w, zp.w)));
+    }
+    st4(zprev_next + p0, zn);
+    bad |= !finite4(zn);
+  }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1);
+}
+
+// Q = sum_j (w_j - z_prev) (Mode B prologue).
+__global__ void __launch_bounds__(kThreads) q_prologue_kernel(const float* __restrict__ W,
+                                                              int64_t ld, int r,
+                                                              const float* __restrict__ zp,
+                                                              float* __restrict__ Q, int64_t n4) {
+  for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < n4;
+       c += (int64_t)gridDim.x * kThreads) {
+    const int64_t p0 = c << 2;
+    const float4 z = ld_ro(zp + p0);
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j = 0; j < r; ++j) {
+      const float4 w = ld_ro(W + (int64_t)j * ld + p0);
+      acc.x = __fadd_rn(acc.x, __fsub_rn(w.x, z.x));
+      acc.y = __fadd_rn(acc.y, __fsub_rn(w.y, z.y));
+      acc.z = __fadd_rn(acc.z, __fsub_rn(w.z, z.z));
+      acc.w = __fadd_rn(acc.w, __fsub_rn(w.w, z.w));
+    }
+    st4(Q + p0, acc);
+  }
+}
+
+// ------------------------------------------------------ synthetic gradients
+// DESIGN.md "Input recipe" (R9), implemented here independently of the oracle.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void __launch_bounds__(kThreads) synth_grads_kernel(float* __restrict__ G, int64_t ld,
+                                                               int r, int j0, int k, int64_t d,
+                                                               int64_t round, uint64_t key) {
+  const int64_t n4 = ld >> 2;
+  const int64_t total = n4 * r;
+  for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * kThreads) {
+    const int slot = (int)(t / n4);
+    const int64_t p0 = (t - (int64_t)slot * n4) << 2;
+    const uint64_t base = ((uint64_t)round * (uint64_t)k + (uint64_t)(j0 + slot)) * (uint64_t)d;
+    float v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t p = p0 + q;
+      const uint64_t h = splitmix64(key + base + (uint64_t)p);
+      // (U - 1/2) 2^-4 with U = (h >> 40) 2^-24: exact in fp32
+      v[q] = (p < d) ? ((float)(h >> 40) * 0x1p-24f - 0.5f) * 0.0625f : 0.f;
+    }
+    st4(G + (int64_t)slot * ld + p0, make_float4(v[0], v[1], v[2], v[3]));
+  }
+}
+
+// ------------------------------------------------ softmax learner (a2')
+// grid (r, kSoftmaxSplit): every CTA of learner `slot` gathers the b rows of
+// its batch into shared memory, computes the b x classes logits (one warp per
+// (row, class) pair, lanes stride the features, xor-shuffle reduction), the
+// max-subtracted softmax and e = p - onehot(y); then it writes the slice
+// blockIdx.y of dW[c][f] = (1/b) sum_t e[t][c] x[t][f] (and db on slice 0).
+// fp32 FFMA throughout (no TF32: SURVEY Appendix A5).
+constexpr int kSoftmaxSplit = 8;
+constexpr int kSoftmaxThreads = 512;
+__global__ void __launch_bounds__(kSoftmaxThreads) softmax_grad_kernel(
+    const float* __restrict__ X, const int32_t* __restrict__ y, const int32_t* __restrict__ perm,
+    int64_t pos0, int b, int in_dim, int classes, const float* __restrict__ Wall, int64_t ld,
+    int j0, float* __restrict__ Gall) {
+  extern __shared__ float smem[];
+  float* xs = smem;                          // [b][in_dim]
+  float* e = xs + (int64_t)b * in_dim;       // [b][classes]
+  int* rows = (int*)(e + b * classes);       // [b]
+  const int slot = blockIdx.x;
+  const float* W = Wall + (int64_t)slot * ld;
+  float* G = Gall + (int64_t)slot * ld;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  if (threadIdx.x < b) rows[threadIdx.x] = perm[pos0 + (int64_t)(j0 + slot) * b + threadIdx.x];
+  __syncthreads();
+  for (int q = threadIdx.x; q < b * in_dim; q += blockDim.x) {
+    const int t = q / in_dim, f = q - t * in_dim;
+    xs[q] = X[(int64_t)rows[t] * in_dim + f];
+  }
+  __syncthreads();
+  const float* bias = W + (int64_t)classes * in_dim;
+  for (int pr = warp; pr < b * classes; pr += nwarps) {
+    const int t = pr / classes, c = pr - t * classes;
+    float s = 0.f;
+    for (int f = lane; f < in_dim; f += 32) s = __fmaf_rn(W[(int64_t)c * in_dim + f], xs[t * in_dim + f], s);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+    if (lane == 0) e[pr] = __fadd_rn(s, bias[c]);
+  }
+  __syncthreads();
+  if (threadIdx.x < b) {  // softmax of row t, then e = p - onehot(y_t)
+    const int t = threadIdx.x;
+    float mx = e[t * classes];
+    for (int c = 1; c < classes; ++c) mx = fmaxf(mx, e[t * classes + c]);
+    float den = 0.f;
+    for (int c = 0; c < classes; ++c) den = __fadd_rn(den, expf(__fsub_rn(e[t * classes + c], mx)));
+    const int yt = y[rows[t]];
+    for (int c = 0; c < classes; ++c) {
+      const float pc = __fdiv_rn(expf(__fsub_rn(e[t * classes + c], mx)), den);
+      e[t * classes + c] = __fsub_rn(pc, c == yt ? 1.f : 0.f);
+    }
+  }
+  __syncthreads();
+  const float fb = (float)b;
+  const int nW = classes * in_dim;
+  const int per = (nW + gridDim.y - 1) / gridDim.y;
+  const int lo = blockIdx.y * per, hi = min(nW, lo + per);
+  for (int q = lo + threadIdx.x; q < hi; q += blockDim.x) {
+    const int c = q / in_dim, f = q - c * in_dim;
+    float s = 0.f;
+    for (int t = 0; t < b; ++t) s = __fmaf_rn(e[t * classes + c], xs[t * in_dim + f], s);
+    G[q] = __fdiv_rn(s, fb);
+  }
+  if (blockIdx.y == 0 && threadIdx.x < classes) {
+    float s = 0.f;
+    for (int t = 0; t < b; ++t) s = __fadd_rn(s, e[t * classes + threadIdx.x]);
+    G[nW + threadIdx.x] = __fdiv_rn(s, fb);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) broadcast_rows_kernel(float* __restrict__ dst, int64_t ld,
+                                                                  int r, const float* __restrict__ src,
+                                                                  int64_t n4) {
+  const int64_t total = n4 * r;
+  for (int64_t t = (int64_t)blockIdx.x * kThreads + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * kThreads) {
+    const int slot = (int)(t / n4);
+    const int64_t p0 = (t - (int64_t)slot * n4) << 2;
+    st4(dst + (int64_t)slot * ld + p0, ld_ro(src + p0));
+  }
+}
+
+template <typename K>
+int grid_for(K kernel, int threads, size_t smem, int64_t work_items, int num_sms) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess ||
+      occ < 1)
+    occ = 1;
+  const int64_t want = (work_items + threads - 1) / threads;
+  const int64_t cap = (int64_t)num_sms * occ;
+  return (int)(want < 1 ? 1 : (want < cap ? want : cap));
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- launchers
+cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a, int num_sms,
+                                cudaStream_t s) {
+  if (tma) return cudaErrorNotSupported;  // TMA variant: see sma_kernels_tma.cu
+  switch (mode) {
+    case kFused: {
+      auto k = replica_step_ldg<kFused>;
+      k<<<grid_for(k, kThreads, 0, a.n4, num_sms), kThreads, 0, s>>>(a);
+      break;
+    }
+    case kPartialA: {
+      auto k = replica_step_ldg<kPartialA>;
+      k<<<grid_for(k, kThreads, 0, a.n4, num_sms), kThreads, 0, s>>>(a);
+      break;
+    }
+    case kPartialB: {
+      auto k = replica_step_ldg<kPartialB>;
+      k<<<grid_for(k, kThreads, 0, a.n4, num_sms), kThreads, 0, s>>>(a);
+      break;
+    }
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_corrections(int mode, const ReplicaArgs& a, int num_sms,
+                                      cudaStream_t s) {
+  const int64_t tiles = (a.n4 + 7) / 8;
+  const int64_t cap = (int64_t)num_sms * 8;
+  const int grid = (int)(tiles < cap ? tiles : cap);
+  if (mode == kFused)
+    reduce_corrections<kFused><<<grid, kRedWarps * 32, 0, s>>>(a);
+  else if (mode == kPartialA)
+    reduce_corrections<kPartialA><<<grid, kRedWarps * 32, 0, s>>>(a);
+  else
+    return cudaErrorInvalidValue;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zsync(int mode, const float* S, const float* z, float* zprev_next, int64_t n4,
+                         float alpha, float mu, float coef_b, int* nonfinite, int num_sms,
+                         cudaStream_t s) {
+  if (mode == kPartialA) {
+    auto k = zsync_kernel<kPartialA>;
+    k<<<grid_for(k, kThreads, 0, n4, num_sms), kThreads, 0, s>>>(S, z, zprev_next, n4, alpha, mu,
+                                                                 coef_b, nonfinite);
+  } else {
+    auto k = zsync_kernel<kPartialB>;
+    k<<<grid_for(k, kThreads, 0, n4, num_sms), kThreads, 0, s>>>(S, z, zprev_next, n4, alpha, mu,
+                                                                 coef_b, nonfinite);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_q_prologue(const float* W, int64_t ld, int r, const float* zprev, float* Q,
+                              int64_t n4, int num_sms, cudaStream_t s) {
+  q_prologue_kernel<<<grid_for(q_prologue_kernel, kThreads, 0, n4, num_sms), kThreads, 0, s>>>(
+      W, ld, r, zprev, Q, n4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth_grads(float* G, int64_t ld, int r, int j0, int k, int64_t d,
+                               int64_t round, uint64_t seed, int num_sms, cudaStream_t s) {
+  // key(seed) = splitmix64(seed), computed on the host side of the launch
+  uint64_t z = seed + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  const uint64_t key = z ^ (z >> 31);
+  synth_grads_kernel<<<grid_for(synth_grads_kernel, kThreads, 0, (ld >> 2) * r, num_sms), kThreads,
+                       0, s>>>(G, ld, r, j0, k, d, round, key);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_softmax_grad(const float* X, const int32_t* y, const int32_t* perm, int64_t pos0,
+                                int b, int in_dim, int classes, const float* W, int64_t ld, int r,
+                                int j0, float* G, cudaStream_t s) {
+  const size_t smem = sizeof(float) * ((size_t)b * in_dim + (size_t)b * classes) + sizeof(int) * b;
+  cudaError_t e = cudaFuncSetAttribute(softmax_grad_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(r, kSoftmaxSplit);
+  softmax_grad_kernel<<<grid, kSoftmaxThreads, smem, s>>>(X, y, perm, pos0, b, in_dim, classes, W,
+                                                          ld, j0, G);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_broadcast_rows(float* dst, int64_t ld, int r, const float* src, int64_t n4,
+                                  int num_sms, cudaStream_t s) {
+  broadcast_rows_kernel<<<grid_for(broadcast_rows_kernel, kThreads, 0, n4 * r, num_sms), kThreads,
+                          0, s>>>(dst, ld, r, src, n4);
+  return cudaGetLastError();
+}
+
+}  // namespace sma

@@ -1,0 +1,820 @@
+// sma_runtime.cu -- libsma's C ABI (include/sma.h): handle, buffers, streams,
+// events, NCCL communicator, CUDA graphs and host bookkeeping.
+//
+// One round (sma_step) is one iteration of Alg. 1.  The
+// runtime replaces Crossbow's task manager/scheduler with a
+// static contiguous layout: the r local replicas live in ONE allocation
+// W[r][d_pad] and are advanced by ONE batched kernel instead
+// of r learner streams; the global synchronisation task
+// is NCCL reduce-scatter -> shard update -> all-gather on
+// the caller's stream (Mode A) or on a second stream overlapping the next
+// replica kernel (Mode B).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <stdint.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "../../include/sma.h"
+#include "sma_internal.h"
+
+using namespace sma;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+static sma_status fail(sma_status st, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+static sma_status fail(sma_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return st;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t _e = (expr);                                                              \
+    if (_e != cudaSuccess)                                                                \
+      return fail(_e == cudaErrorMemoryAllocation ? SMA_ERR_OOM : SMA_ERR_CUDA,           \
+                  "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+#define STATUS_TRY(expr)              \
+  do {                                \
+    sma_status _s = (expr);           \
+    if (_s != SMA_OK) return _s;      \
+  } while (0)
+
+// ------------------------------------------------------ NCCL (dlopen'ed)
+// libsma does not link NCCL: it binds the few entry points it needs from the
+// process's libnccl.so.2 (the one torch already loaded, else the system one),
+// so a single-GPU process never needs NCCL and there is one NCCL per process.
+namespace {
+struct NcclApi {
+  bool tried = false, ok = false;
+  std::string why;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+  ncclResult_t (*ReduceScatter)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t,
+                                ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool nccl_load() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) {
+    g_nccl.why = dlerror() ? dlerror() : "libnccl.so.2 not found";
+    return false;
+  }
+#define BIND(field, sym)                                                       \
+  g_nccl.field = reinterpret_cast<decltype(g_nccl.field)>(dlsym(h, sym));      \
+  if (!g_nccl.field) {                                                         \
+    g_nccl.why = std::string("missing symbol ") + sym;                         \
+    return false;                                                              \
+  }
+  BIND(GetUniqueId, "ncclGetUniqueId");
+  BIND(CommInitRank, "ncclCommInitRank");
+  BIND(CommDestroy, "ncclCommDestroy");
+  BIND(CommAbort, "ncclCommAbort");
+  BIND(ReduceScatter, "ncclReduceScatter");
+  BIND(AllGather, "ncclAllGather");
+  BIND(GetErrorString, "ncclGetErrorString");
+#undef BIND
+  g_nccl.ok = true;
+  return true;
+}
+}  // namespace
+
+#define NCCL_TRY(expr)                                                                  \
+  do {                                                                                  \
+    ncclResult_t _r = (expr);                                                           \
+    if (_r != ncclSuccess)                                                              \
+      return fail(SMA_ERR_NCCL, "%s failed: %s", #expr, g_nccl.GetErrorString(_r));     \
+  } while (0)
+
+// --------------------------------------------------- host bookkeeping
+// Independent of the oracle's implementation (tests compare the two bit-exactly).
+static uint64_t host_splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+extern "C" int64_t sma_plan_d_pad(int64_t d, int32_t world) {
+  if (d < 1 || world < 1) return -1;
+  int64_t a = 512, b = 64LL * world;  // lcm(512, 64 n)
+  int64_t x = a, y = b;
+  while (y) { int64_t t = x % y; x = y; y = t; }
+  const int64_t l = a / x * b;
+  return (d + l - 1) / l * l;
+}
+
+extern "C" sma_status sma_plan_local_replicas(int32_t k, int32_t world, int32_t rank,
+                                              int32_t* first, int32_t* count) {
+  if (k < 1 || world < 1 || rank < 0 || rank >= world || !first || !count)
+    return fail(SMA_ERR_INVALID_ARG, "sma_plan_local_replicas: bad arguments");
+  const int64_t lo = (int64_t)rank * k / world, hi = (int64_t)(rank + 1) * k / world;
+  *first = (int32_t)lo;
+  *count = (int32_t)(hi - lo);
+  return SMA_OK;
+}
+
+extern "C" sma_status sma_plan_replica_location(int32_t k, int32_t world, int32_t j,
+                                                int32_t* rank, int32_t* slot) {
+  if (k < 1 || world < 1 || j < 0 || j >= k || !rank || !slot)
+    return fail(SMA_ERR_INVALID_ARG, "sma_plan_replica_location: j=%d outside [0,%d)", j, k);
+  // floor(g k / n) <= j  <=>  g <= (j n + n - 1) / k ... take the largest such g
+  int32_t g = (int32_t)(((int64_t)j * world + world - 1) / k);
+  if (g >= world) g = world - 1;
+  while (g > 0 && (int64_t)g * k / world > j) --g;
+  while ((int64_t)(g + 1) * k / world <= j) ++g;
+  *rank = g;
+  *slot = (int32_t)(j - (int64_t)g * k / world);
+  return SMA_OK;
+}
+
+extern "C" sma_status sma_plan_shard_range(int64_t d, int32_t world, int32_t rank,
+                                           int64_t* offset, int64_t* length) {
+  if (d < 1 || world < 1 || rank < 0 || rank >= world || !offset || !length)
+    return fail(SMA_ERR_INVALID_ARG, "sma_plan_shard_range: bad arguments");
+  const int64_t len = sma_plan_d_pad(d, world) / world;
+  *offset = rank * len;
+  *length = len;
+  return SMA_OK;
+}
+
+// Fisher-Yates permutation of [0, N) for `epoch` (reading R10), int32 output.
+static void plan_epoch_permutation(int64_t N, uint64_t seed, int64_t epoch, int32_t* perm) {
+  for (int64_t t = 0; t < N; ++t) perm[t] = (int32_t)t;
+  const uint64_t key = host_splitmix64(seed ^ (uint64_t)epoch);
+  for (int64_t t = N - 1; t > 0; --t) {
+    const uint64_t u = host_splitmix64(key + (uint64_t)t);
+    const int64_t r = (int64_t)(((unsigned __int128)u * (uint64_t)(t + 1)) >> 64);
+    const int32_t tmp = perm[t];
+    perm[t] = perm[r];
+    perm[r] = tmp;
+  }
+}
+
+extern "C" sma_status sma_plan_batch_indices(int64_t n_samples, int32_t k, int32_t batch,
+                                             uint64_t batch_seed, int64_t round, int32_t j,
+                                             int64_t* out) {
+  if (n_samples < 1 || n_samples > INT32_MAX || k < 1 || batch < 1 || round < 0 || j < 0 ||
+      j >= k || !out)
+    return fail(SMA_ERR_INVALID_ARG, "sma_plan_batch_indices: bad arguments");
+  const int64_t E = n_samples / ((int64_t)k * batch);
+  if (E < 1) return fail(SMA_ERR_INVALID_ARG, "n_samples < k*batch");
+  std::vector<int32_t> perm((size_t)n_samples);
+  plan_epoch_permutation(n_samples, batch_seed, round / E, perm.data());
+  const int64_t base = ((round % E) * k + j) * (int64_t)batch;
+  for (int32_t t = 0; t < batch; ++t) out[t] = perm[(size_t)(base + t)];
+  return SMA_OK;
+}
+
+// ------------------------------------------------------------------ handle
+struct sma_handle {
+  sma_config cfg{};
+  int dev = 0, num_sms = 148;
+  int64_t d_pad = 0, n4 = 0, shard_off = 0, shard_len = 0;
+  int r = 0, j0 = 0;
+  bool collective = false, overlap = false, matc = false, tma = false, timing = false,
+       graphs = false, check = false;
+  float alpha = 0, gamma = 0, mu = 0;
+
+  float* W = nullptr;      // [r][d_pad]
+  float* zbuf = nullptr;   // [2][d_pad]
+  float* P = nullptr;      // [d_pad] per-GPU partial (collective, Mode A)
+  float* S = nullptr;      // [shard] reduce-scatter result
+  float* Q = nullptr;      // [2][d_pad] (Mode B)
+  float* C = nullptr;      // [r][d_pad] (MATERIALIZE_C)
+  float* G = nullptr;      // [r][d_pad] internal gradient buffers (lazy)
+  int* nonfinite = nullptr;
+  int cur = 0, qi = 0;
+  bool q_dirty = true;
+
+  const float* gptr[SMA_MAX_LOCAL_REPLICAS] = {};
+  uint64_t ver = 1;  // bumps when anything baked into a graph changes
+
+  ncclComm_t comm = nullptr;
+  cudaStream_t sB = nullptr, sIO = nullptr;
+  cudaEvent_t evFork = nullptr, evJoin = nullptr, evDone = nullptr;
+  bool any_work = false;
+
+  cudaGraphExec_t gexec[2] = {nullptr, nullptr};
+  uint64_t gver[2] = {0, 0};
+
+  std::vector<cudaEvent_t> tev;  // (start, stop) pairs
+  size_t tused = 0;
+  int64_t launches = 0;
+
+  // learner
+  bool learner = false;
+  int in_dim = 0, classes = 0, batch = 0;
+  const float* X = nullptr;
+  const int32_t* y = nullptr;
+  int64_t n_samples = 0;
+  uint64_t batch_seed = 0;
+  int32_t* perm_dev[2] = {nullptr, nullptr};
+  int64_t perm_epoch[2] = {-1, -1};
+  int32_t* perm_host = nullptr;
+
+  float* z() const { return zbuf + (int64_t)cur * d_pad; }
+  float* zprev() const { return zbuf + (int64_t)(1 - cur) * d_pad; }
+};
+
+namespace {
+struct DeviceGuard {
+  int old = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&old) != cudaSuccess) old = -1;
+    if (old != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int now = -1;
+    if (old >= 0 && cudaGetDevice(&now) == cudaSuccess && now != old) cudaSetDevice(old);
+  }
+};
+
+bool finite_f(float v) { return std::isfinite(v); }
+
+sma_status local_slot(const sma_handle* h, int32_t j, int* slot) {
+  if (j < 0 || j >= h->cfg.k) return fail(SMA_ERR_INVALID_ARG, "replica %d outside [0,%d)", j, h->cfg.k);
+  if (j < h->j0 || j >= h->j0 + h->r)
+    return fail(SMA_ERR_NOT_LOCAL, "replica %d lives on another rank (local [%d,%d))", j, h->j0,
+                h->j0 + h->r);
+  *slot = j - h->j0;
+  return SMA_OK;
+}
+
+void free_all(sma_handle* h) {
+  DeviceGuard g(h->dev);
+  if (h->any_work) cudaDeviceSynchronize();
+  for (int i = 0; i < 2; ++i)
+    if (h->gexec[i]) cudaGraphExecDestroy(h->gexec[i]);
+  if (h->comm) g_nccl.CommDestroy(h->comm);
+  for (cudaEvent_t e : h->tev) cudaEventDestroy(e);
+  if (h->evFork) cudaEventDestroy(h->evFork);
+  if (h->evJoin) cudaEventDestroy(h->evJoin);
+  if (h->evDone) cudaEventDestroy(h->evDone);
+  if (h->sB) cudaStreamDestroy(h->sB);
+  if (h->sIO) cudaStreamDestroy(h->sIO);
+  cudaFree(h->W);
+  cudaFree(h->zbuf);
+  cudaFree(h->P);
+  cudaFree(h->S);
+  cudaFree(h->Q);
+  cudaFree(h->C);
+  cudaFree(h->G);
+  cudaFree(h->nonfinite);
+  for (int i = 0; i < 2; ++i) cudaFree(h->perm_dev[i]);
+  if (h->perm_host) cudaFreeHost(h->perm_host);
+  delete h;
+}
+
+sma_status ensure_G(sma_handle* h) {
+  if (h->G) return SMA_OK;
+  CUDA_TRY(cudaMalloc(&h->G, sizeof(float) * (size_t)h->r * h->d_pad));
+  CUDA_TRY(cudaMemset(h->G, 0, sizeof(float) * (size_t)h->r * h->d_pad));
+  return SMA_OK;
+}
+
+void set_gptr(sma_handle* h, int slot, const float* p) {
+  if (h->gptr[slot] != p) {
+    h->gptr[slot] = p;
+    ++h->ver;
+  }
+}
+
+sma_status mark_done(sma_handle* h, cudaStream_t s) {
+  CUDA_TRY(cudaEventRecord(h->evDone, s));
+  h->any_work = true;
+  return SMA_OK;
+}
+
+// Wait for everything the handle enqueued, on the host.
+sma_status sync_handle(sma_handle* h) {
+  if (h->any_work) CUDA_TRY(cudaEventSynchronize(h->evDone));
+  return SMA_OK;
+}
+
+sma_status check_nonfinite(sma_handle* h) {
+  if (!h->check) return SMA_OK;
+  int flag = 0;
+  CUDA_TRY(cudaMemcpy(&flag, h->nonfinite, sizeof(int), cudaMemcpyDeviceToHost));
+  if (flag) return fail(SMA_ERR_NONFINITE, "a non-finite value was produced by an SMA round");
+  return SMA_OK;
+}
+
+sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s) {
+  ReplicaArgs a{};
+  a.W = h->W;
+  a.ld = h->d_pad;
+  a.r = h->r;
+  for (int i = 0; i < h->r; ++i) a.g.p[i] = h->gptr[i];
+  a.d = h->cfg.d;
+  a.n4 = h->n4;
+  a.z = h->z();
+  a.zprev_next = h->zprev();
+  a.out = out;
+  a.C = h->matc ? h->C : nullptr;
+  a.alpha = h->alpha;
+  a.gamma = h->gamma;
+  a.mu = h->mu;
+  a.nonfinite = h->check ? h->nonfinite : nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->timing) {
+    if (h->tused + 2 > h->tev.size()) {
+      for (int i = 0; i < 2; ++i) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreate(&e));
+        h->tev.push_back(e);
+      }
+    }
+    e0 = h->tev[h->tused];
+    e1 = h->tev[h->tused + 1];
+    h->tused += 2;
+    CUDA_TRY(cudaEventRecord(e0, s));
+  }
+  if (h->r > 0) {
+    CUDA_TRY(launch_replica_step(mode, h->tma, a, h->num_sms, s));
+    ++h->launches;
+    if (h->matc) {
+      CUDA_TRY(launch_reduce_corrections(mode, a, h->num_sms, s));
+      ++h->launches;
+    }
+  } else if (mode == kFused) {
+    return fail(SMA_ERR_STATE, "no local replicas on a single-rank handle");
+  } else {
+    CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * h->d_pad, s));
+  }
+  if (h->timing) CUDA_TRY(cudaEventRecord(e1, s));
+  return SMA_OK;
+}
+
+// The body of one round, enqueued on stream s (capturable).
+sma_status enqueue_round(sma_handle* h, cudaStream_t s) {
+  const size_t cnt = (size_t)h->shard_len;
+  if (!h->collective) {  // n == 1: a3-a7 fused in one kernel
+    STATUS_TRY(replica_launch(h, kFused, nullptr, s));
+  } else if (!h->overlap) {  // Mode A: paper order (fig:dependencies d/e)
+    STATUS_TRY(replica_launch(h, kPartialA, h->P, s));
+    NCCL_TRY(g_nccl.ReduceScatter(h->P, h->S, cnt, ncclFloat32, ncclSum, h->comm, s));
+    CUDA_TRY(launch_zsync(kPartialA, h->S, h->z() + h->shard_off, h->zprev() + h->shard_off,
+                          h->shard_len / 4, h->alpha, h->mu, 0.f,
+                          h->check ? h->nonfinite : nullptr, h->num_sms, s));
+    NCCL_TRY(g_nccl.AllGather(h->zprev() + h->shard_off, h->zprev(), cnt, ncclFloat32, h->comm, s));
+    h->launches += 1;  // zsync (NCCL's own kernels are not counted)
+  } else {  // Mode B: z-sync(i) on sB  ||  replica kernel(i) on s
+    float* Qcur = h->Q + (int64_t)h->qi * h->d_pad;
+    float* Qnext = h->Q + (int64_t)(1 - h->qi) * h->d_pad;
+    const float coef_b = h->mu - h->alpha * (float)h->cfg.k;
+    CUDA_TRY(cudaEventRecord(h->evFork, s));
+    CUDA_TRY(cudaStreamWaitEvent(h->sB, h->evFork, 0));
+    NCCL_TRY(g_nccl.ReduceScatter(Qcur, h->S, cnt, ncclFloat32, ncclSum, h->comm, h->sB));
+    CUDA_TRY(launch_zsync(kPartialB, h->S, h->z() + h->shard_off, h->zprev() + h->shard_off,
+                          h->shard_len / 4, h->alpha, h->mu, coef_b,
+                          h->check ? h->nonfinite : nullptr, h->num_sms, h->sB));
+    NCCL_TRY(g_nccl.AllGather(h->zprev() + h->shard_off, h->zprev(), cnt, ncclFloat32, h->comm,
+                              h->sB));
+    CUDA_TRY(cudaEventRecord(h->evJoin, h->sB));
+    STATUS_TRY(replica_launch(h, kPartialB, Qnext, s));
+    CUDA_TRY(cudaStreamWaitEvent(s, h->evJoin, 0));
+    h->launches += 1;  // zsync
+  }
+  return SMA_OK;
+}
+
+void advance(sma_handle* h) {
+  h->cur ^= 1;
+  if (h->overlap) h->qi ^= 1;
+}
+
+sma_status alloc_zero(float** p, size_t n) {
+  CUDA_TRY(cudaMalloc(p, sizeof(float) * n));
+  CUDA_TRY(cudaMemset(*p, 0, sizeof(float) * n));
+  return SMA_OK;
+}
+
+sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
+  h->cfg = *cfg;
+  h->dev = cfg->device;
+  h->alpha = cfg->alpha;
+  h->gamma = cfg->gamma;
+  h->mu = cfg->mu;
+  const uint32_t f = cfg->flags;
+  h->collective = cfg->world > 1 || (f & SMA_FLAG_FORCE_COLLECTIVE);
+  h->overlap = h->collective && (f & SMA_FLAG_OVERLAP);
+  h->matc = (f & SMA_FLAG_MATERIALIZE_C) != 0;
+  h->tma = (f & SMA_FLAG_KERNEL_TMA) != 0;
+  h->timing = (f & SMA_FLAG_TIMING) != 0;
+  h->graphs = (f & SMA_FLAG_CUDA_GRAPH) != 0 && !h->timing;
+  h->check = (f & SMA_FLAG_CHECK_FINITE) != 0;
+  h->d_pad = sma_plan_d_pad(cfg->d, cfg->world);
+  h->n4 = h->d_pad / 4;
+  STATUS_TRY(sma_plan_local_replicas(cfg->k, cfg->world, cfg->rank, &h->j0, &h->r));
+  STATUS_TRY(sma_plan_shard_range(cfg->d, cfg->world, cfg->rank, &h->shard_off, &h->shard_len));
+  if (h->r > SMA_MAX_LOCAL_REPLICAS)
+    return fail(SMA_ERR_INVALID_ARG, "%d replicas on rank %d exceeds SMA_MAX_LOCAL_REPLICAS=%d",
+                h->r, cfg->rank, SMA_MAX_LOCAL_REPLICAS);
+  if (h->matc && h->overlap)
+    return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_MATERIALIZE_C is not combined with SMA_FLAG_OVERLAP");
+
+  int ndev = 0;
+  CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (cfg->device < 0 || cfg->device >= ndev)
+    return fail(SMA_ERR_INVALID_ARG, "device %d not present (%d devices)", cfg->device, ndev);
+  DeviceGuard guard(h->dev);
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, h->dev));
+  if (prop.major < 10)
+    return fail(SMA_ERR_CUDA, "device %d is sm_%d%d; libsma is built for sm_100a only", h->dev,
+                prop.major, prop.minor);
+  h->num_sms = prop.multiProcessorCount;
+
+  const size_t dp = (size_t)h->d_pad;
+  STATUS_TRY(alloc_zero(&h->W, dp * (h->r > 0 ? h->r : 1)));
+  STATUS_TRY(alloc_zero(&h->zbuf, 2 * dp));
+  if (h->collective) {
+    STATUS_TRY(alloc_zero(&h->S, (size_t)h->shard_len));
+    if (h->overlap)
+      STATUS_TRY(alloc_zero(&h->Q, 2 * dp));
+    else
+      STATUS_TRY(alloc_zero(&h->P, dp));
+  }
+  if (h->matc) STATUS_TRY(alloc_zero(&h->C, dp * (h->r > 0 ? h->r : 1)));
+  CUDA_TRY(cudaMalloc(&h->nonfinite, sizeof(int)));
+  CUDA_TRY(cudaMemset(h->nonfinite, 0, sizeof(int)));
+  CUDA_TRY(cudaStreamCreateWithFlags(&h->sB, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&h->sIO, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&h->evFork, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&h->evJoin, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventCreateWithFlags(&h->evDone, cudaEventDisableTiming));
+
+  // Alg. 1 line 1-2 (R2) and R3: z = z_prev = w_j = w0; padding stays 0.
+  CUDA_TRY(cudaMemcpy(h->zbuf, w0, sizeof(float) * cfg->d, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(h->zbuf + dp, h->zbuf, sizeof(float) * dp, cudaMemcpyDeviceToDevice));
+  if (h->r > 0) CUDA_TRY(launch_broadcast_rows(h->W, h->d_pad, h->r, h->zbuf, h->n4, h->num_sms, 0));
+  CUDA_TRY(cudaDeviceSynchronize());
+
+  if (h->collective) {
+    if (!nccl_load()) return fail(SMA_ERR_NCCL, "cannot load NCCL: %s", g_nccl.why.c_str());
+    ncclUniqueId id;
+    if (cfg->world > 1) {
+      memcpy(&id, cfg->nccl_id, sizeof id);
+    } else {
+      NCCL_TRY(g_nccl.GetUniqueId(&id));
+    }
+    NCCL_TRY(g_nccl.CommInitRank(&h->comm, cfg->world, id, cfg->rank));
+  }
+  return SMA_OK;
+}
+}  // namespace
+
+// ======================================================================= ABI
+extern "C" {
+
+int sma_abi_version(void) { return SMA_ABI_VERSION; }
+const char* sma_last_error(void) { return g_last_error.c_str(); }
+
+sma_status sma_nccl_unique_id(void* out) {
+  if (!out) return fail(SMA_ERR_INVALID_ARG, "NULL output");
+  if (!nccl_load()) return fail(SMA_ERR_NCCL, "cannot load NCCL: %s", g_nccl.why.c_str());
+  ncclUniqueId id;
+  NCCL_TRY(g_nccl.GetUniqueId(&id));
+  memcpy(out, &id, sizeof id);
+  return SMA_OK;
+}
+
+sma_status sma_create(const sma_config* cfg, const float* w0_host, sma_handle** out) {
+  if (!out) return fail(SMA_ERR_INVALID_ARG, "NULL out");
+  *out = nullptr;
+  if (!cfg || !w0_host) return fail(SMA_ERR_INVALID_ARG, "NULL config or w0");
+  if (cfg->d < 1) return fail(SMA_ERR_INVALID_ARG, "d must be >= 1 (got %lld)", (long long)cfg->d);
+  if (cfg->k < 1) return fail(SMA_ERR_INVALID_ARG, "k must be >= 1 (got %d)", cfg->k);
+  if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world)
+    return fail(SMA_ERR_INVALID_ARG, "bad rank/world %d/%d", cfg->rank, cfg->world);
+  if (!finite_f(cfg->alpha) || !finite_f(cfg->gamma) || !finite_f(cfg->mu))
+    return fail(SMA_ERR_INVALID_ARG, "non-finite hyper-parameter");
+  if (cfg->world > 1 && !cfg->nccl_id)
+    return fail(SMA_ERR_INVALID_ARG, "world > 1 requires nccl_id");
+  sma_handle* h = new sma_handle();
+  sma_status st = create_impl(cfg, w0_host, h);
+  if (st != SMA_OK) {
+    std::string msg = g_last_error;
+    free_all(h);
+    g_last_error = msg;
+    return st;
+  }
+  *out = h;
+  return SMA_OK;
+}
+
+void sma_destroy(sma_handle* h) {
+  if (h) free_all(h);
+}
+
+sma_status sma_set_learner_grads(sma_handle* h, int32_t j, const float* g_dev) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  int slot;
+  STATUS_TRY(local_slot(h, j, &slot));
+  if (!g_dev || (reinterpret_cast<uintptr_t>(g_dev) & 15u))
+    return fail(SMA_ERR_INVALID_ARG, "gradient pointer must be non-NULL and 16-byte aligned");
+  set_gptr(h, slot, g_dev);
+  return SMA_OK;
+}
+
+sma_status sma_set_learner_grads_host(sma_handle* h, int32_t j, const float* g_host, void* stream) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  int slot;
+  STATUS_TRY(local_slot(h, j, &slot));
+  if (!g_host) return fail(SMA_ERR_INVALID_ARG, "NULL gradient");
+  DeviceGuard guard(h->dev);
+  STATUS_TRY(ensure_G(h));
+  cudaStream_t s = (cudaStream_t)stream;
+  float* dst = h->G + (int64_t)slot * h->d_pad;
+  CUDA_TRY(cudaMemcpyAsync(dst, g_host, sizeof(float) * h->cfg.d, cudaMemcpyHostToDevice, s));
+  set_gptr(h, slot, dst);
+  return mark_done(h, s);
+}
+
+sma_status sma_synth_grads(sma_handle* h, int64_t round, uint64_t seed, void* stream) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (round < 0) return fail(SMA_ERR_INVALID_ARG, "round < 0");
+  if (h->r == 0) return SMA_OK;
+  DeviceGuard guard(h->dev);
+  STATUS_TRY(ensure_G(h));
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(launch_synth_grads(h->G, h->d_pad, h->r, h->j0, h->cfg.k, h->cfg.d, round, seed,
+                              h->num_sms, s));
+  ++h->launches;
+  for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
+  return mark_done(h, s);
+}
+
+sma_status sma_step(sma_handle* h, void* stream) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  for (int i = 0; i < h->r; ++i)
+    if (!h->gptr[i])
+      return fail(SMA_ERR_GRADS_MISSING, "learner %d has no registered gradient", h->j0 + i);
+  DeviceGuard guard(h->dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (h->overlap && h->q_dirty) {
+    CUDA_TRY(launch_q_prologue(h->W, h->d_pad, h->r, h->zprev(), h->Q + (int64_t)h->qi * h->d_pad,
+                               h->n4, h->num_sms, s));
+    ++h->launches;
+    h->q_dirty = false;
+  }
+  if (h->graphs && s != nullptr) {
+    const int key = h->cur;
+    if (!h->gexec[key] || h->gver[key] != h->ver) {
+      const int64_t launches0 = h->launches;
+      cudaGraph_t graph = nullptr;
+      CUDA_TRY(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+      sma_status st = enqueue_round(h, s);
+      cudaError_t ce = cudaStreamEndCapture(s, &graph);
+      h->launches = launches0;
+      if (st != SMA_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      if (ce != cudaSuccess)
+        return fail(SMA_ERR_CUDA, "graph capture failed: %s", cudaGetErrorString(ce));
+      if (h->gexec[key]) {
+        cudaGraphExecDestroy(h->gexec[key]);
+        h->gexec[key] = nullptr;
+      }
+      ce = cudaGraphInstantiate(&h->gexec[key], graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess)
+        return fail(SMA_ERR_CUDA, "graph instantiate failed: %s", cudaGetErrorString(ce));
+      h->gver[key] = h->ver;
+    }
+    CUDA_TRY(cudaGraphLaunch(h->gexec[key], s));
+    h->launches += (h->collective ? 2 : 1) + (h->matc ? 1 : 0);
+  } else {
+    STATUS_TRY(enqueue_round(h, s));
+  }
+  advance(h);
+  return mark_done(h, s);
+}
+
+static sma_status copy_out(sma_handle* h, const float* src, float* out, int out_is_device) {
+  if (!out) return fail(SMA_ERR_INVALID_ARG, "NULL output");
+  DeviceGuard guard(h->dev);
+  STATUS_TRY(sync_handle(h));
+  CUDA_TRY(cudaMemcpyAsync(out, src, sizeof(float) * h->cfg.d,
+                           out_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->sIO));
+  CUDA_TRY(cudaStreamSynchronize(h->sIO));
+  return check_nonfinite(h);
+}
+
+sma_status sma_get_central(sma_handle* h, float* z_out, int out_is_device) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  return copy_out(h, h->z(), z_out, out_is_device);
+}
+
+sma_status sma_get_central_prev(sma_handle* h, float* out, int out_is_device) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  return copy_out(h, h->zprev(), out, out_is_device);
+}
+
+sma_status sma_get_replica(sma_handle* h, int32_t j, float* out, int out_is_device) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  int slot;
+  STATUS_TRY(local_slot(h, j, &slot));
+  return copy_out(h, h->W + (int64_t)slot * h->d_pad, out, out_is_device);
+}
+
+static sma_status copy_in(sma_handle* h, float* dst, const float* src, int in_is_device) {
+  CUDA_TRY(cudaMemcpyAsync(dst, src, sizeof(float) * h->cfg.d,
+                           in_is_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->sIO));
+  return SMA_OK;
+}
+
+sma_status sma_set_replica(sma_handle* h, int32_t j, const float* w, int in_is_device) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  int slot;
+  STATUS_TRY(local_slot(h, j, &slot));
+  if (!w) return fail(SMA_ERR_INVALID_ARG, "NULL input");
+  DeviceGuard guard(h->dev);
+  STATUS_TRY(sync_handle(h));
+  STATUS_TRY(copy_in(h, h->W + (int64_t)slot * h->d_pad, w, in_is_device));
+  CUDA_TRY(cudaStreamSynchronize(h->sIO));
+  h->q_dirty = true;
+  return SMA_OK;
+}
+
+sma_status sma_set_central(sma_handle* h, const float* z, const float* z_prev, int in_is_device) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (!z || !z_prev) return fail(SMA_ERR_INVALID_ARG, "NULL input");
+  DeviceGuard guard(h->dev);
+  STATUS_TRY(sync_handle(h));
+  STATUS_TRY(copy_in(h, h->z(), z, in_is_device));
+  STATUS_TRY(copy_in(h, h->zprev(), z_prev, in_is_device));
+  CUDA_TRY(cudaStreamSynchronize(h->sIO));
+  h->q_dirty = true;
+  return SMA_OK;
+}
+
+sma_status sma_replica_device_ptr(sma_handle* h, int32_t j, const float** w_dev) {
+  if (!h || !w_dev) return fail(SMA_ERR_INVALID_ARG, "NULL argument");
+  int slot;
+  STATUS_TRY(local_slot(h, j, &slot));
+  *w_dev = h->W + (int64_t)slot * h->d_pad;
+  return SMA_OK;
+}
+
+sma_status sma_central_device_ptr(sma_handle* h, const float** z_dev) {
+  if (!h || !z_dev) return fail(SMA_ERR_INVALID_ARG, "NULL argument");
+  *z_dev = h->z();
+  return SMA_OK;
+}
+
+sma_status sma_restart(sma_handle* h, void* stream) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  DeviceGuard guard(h->dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  // Alg. 1 again with w0 := z; z_prev := z.
+  CUDA_TRY(cudaMemcpyAsync(h->zprev(), h->z(), sizeof(float) * h->d_pad, cudaMemcpyDeviceToDevice, s));
+  if (h->r > 0) {
+    CUDA_TRY(launch_broadcast_rows(h->W, h->d_pad, h->r, h->z(), h->n4, h->num_sms, s));
+    ++h->launches;
+  }
+  h->q_dirty = true;
+  return mark_done(h, s);
+}
+
+sma_status sma_set_hparams(sma_handle* h, float alpha, float gamma, float mu) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (!finite_f(alpha) || !finite_f(gamma) || !finite_f(mu))
+    return fail(SMA_ERR_INVALID_ARG, "non-finite hyper-parameter");
+  h->alpha = alpha;
+  h->gamma = gamma;
+  h->mu = mu;
+  ++h->ver;
+  return SMA_OK;
+}
+
+sma_status sma_check_finite(sma_handle* h, int* flag) {
+  if (!h || !flag) return fail(SMA_ERR_INVALID_ARG, "NULL argument");
+  DeviceGuard guard(h->dev);
+  STATUS_TRY(sync_handle(h));
+  CUDA_TRY(cudaMemcpy(flag, h->nonfinite, sizeof(int), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemset(h->nonfinite, 0, sizeof(int)));
+  return SMA_OK;
+}
+
+sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32_t hidden,
+                              int32_t classes, int32_t batch, const float* X_dev,
+                              const int32_t* y_dev, int64_t n_samples, uint64_t batch_seed) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  (void)hidden;
+  if (kind != 0) return fail(SMA_ERR_INVALID_ARG, "learner kind %d not available (0 = softmax)", kind);
+  if (in_dim < 1 || classes < 2 || batch < 1 || batch > 64 || !X_dev || !y_dev)
+    return fail(SMA_ERR_INVALID_ARG, "bad learner arguments");
+  if ((int64_t)classes * in_dim + classes != h->cfg.d)
+    return fail(SMA_ERR_INVALID_ARG, "d=%lld != classes*in_dim+classes=%lld", (long long)h->cfg.d,
+                (long long)classes * in_dim + classes);
+  if (n_samples < (int64_t)h->cfg.k * batch || n_samples > INT32_MAX)
+    return fail(SMA_ERR_INVALID_ARG, "n_samples must be in [k*batch, 2^31)");
+  if ((size_t)batch * in_dim * sizeof(float) > 200 * 1024)
+    return fail(SMA_ERR_INVALID_ARG, "batch*in_dim too large for shared memory");
+  DeviceGuard guard(h->dev);
+  STATUS_TRY(sync_handle(h));
+  for (int i = 0; i < 2; ++i) {
+    cudaFree(h->perm_dev[i]);
+    h->perm_dev[i] = nullptr;
+    h->perm_epoch[i] = -1;
+    CUDA_TRY(cudaMalloc(&h->perm_dev[i], sizeof(int32_t) * (size_t)n_samples));
+  }
+  if (h->perm_host) cudaFreeHost(h->perm_host);
+  h->perm_host = nullptr;
+  CUDA_TRY(cudaMallocHost(&h->perm_host, sizeof(int32_t) * (size_t)n_samples));
+  STATUS_TRY(ensure_G(h));
+  h->learner = true;
+  h->in_dim = in_dim;
+  h->classes = classes;
+  h->batch = batch;
+  h->X = X_dev;
+  h->y = y_dev;
+  h->n_samples = n_samples;
+  h->batch_seed = batch_seed;
+  return SMA_OK;
+}
+
+sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (!h->learner) return fail(SMA_ERR_STATE, "no learner attached");
+  if (round < 0) return fail(SMA_ERR_INVALID_ARG, "round < 0");
+  if (h->r == 0) return SMA_OK;
+  DeviceGuard guard(h->dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t E = h->n_samples / ((int64_t)h->cfg.k * h->batch);
+  const int64_t e = round / E;
+  const int buf = (int)(e & 1);
+  if (h->perm_epoch[buf] != e) {
+    // new epoch: build pi_e on the host (R10) and upload it; the pinned
+    // staging buffer is reused only after the previous upload completed.
+    STATUS_TRY(sync_handle(h));
+    plan_epoch_permutation(h->n_samples, h->batch_seed, e, h->perm_host);
+    CUDA_TRY(cudaMemcpyAsync(h->perm_dev[buf], h->perm_host, sizeof(int32_t) * h->n_samples,
+                             cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    h->perm_epoch[buf] = e;
+  }
+  const int64_t pos0 = (round % E) * h->cfg.k * (int64_t)h->batch;
+  CUDA_TRY(launch_softmax_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim, h->classes,
+                               h->W, h->d_pad, h->r, h->j0, h->G, s));
+  ++h->launches;
+  for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
+  return mark_done(h, s);
+}
+
+sma_status sma_kernel_time(sma_handle* h, double* total_ms, int64_t* launches, int reset) {
+  if (!h || !total_ms || !launches) return fail(SMA_ERR_INVALID_ARG, "NULL argument");
+  DeviceGuard guard(h->dev);
+  STATUS_TRY(sync_handle(h));
+  double tot = 0;
+  for (size_t i = 0; i + 1 < h->tused; i += 2) {
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, h->tev[i], h->tev[i + 1]));
+    tot += ms;
+  }
+  *total_ms = tot;
+  *launches = (int64_t)(h->tused / 2);
+  if (reset) h->tused = 0;
+  return SMA_OK;
+}
+
+int64_t sma_launch_count(const sma_handle* h) { return h ? h->launches : -1; }
+
+sma_status sma_info(const sma_handle* h, int64_t* d_pad, int32_t* local_first, int32_t* local_count,
+                    int64_t* shard_offset, int64_t* shard_length) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (d_pad) *d_pad = h->d_pad;
+  if (local_first) *local_first = h->j0;
+  if (local_count) *local_count = h->r;
+  if (shard_offset) *shard_offset = h->shard_off;
+  if (shard_length) *shard_length = h->shard_len;
+  return SMA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,335 @@
+"""GPU parity: libsma (through the C ABI) vs the fp64 oracle on the same seeded
+inputs.  Bar (north_star): max |err| <= 1e-5 (1 + |ref|) after 100 rounds on z
+and every replica; bitwise where the arithmetic is exact (dyadic traces,
+alpha = 0, generator, padding, bookkeeping)."""
+import numpy as np
+import pytest
+
+import sma_inputs
+from oracle import exact
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+F32 = lambda x: float(np.float32(x))  # noqa: E731
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device (no fallback)"
+    torch.cuda.set_device(0)
+    return torch
+
+
+@pytest.fixture(scope="module")
+def S():
+    from paper_1901_02244_b200 import sma
+    sma.load()
+    return sma
+
+
+def relerr(got, ref):
+    got = np.asarray(got, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.max(np.abs(got - ref) / (1.0 + np.abs(ref)))) if ref.size else 0.0
+
+
+COLLECTIVE_FLAGS = {
+    "fused": 0,
+    "fused_graph": 8,
+    "matc": 2,
+    "collA": 16,
+    "collA_graph": 16 | 8,
+    "collA_matc": 16 | 2,
+    "collB": 16 | 1,
+    "collB_graph": 16 | 1 | 8,
+}
+
+
+def dev_read(ptr, n):
+    """Copy n floats from a raw device pointer to host (cudart of this process)."""
+    import ctypes
+    import torch
+    torch.cuda.synchronize()
+    rt = ctypes.CDLL("libcudart.so.12")
+    out = np.empty(n, np.float32)
+    rc = rt.cudaMemcpy(ctypes.c_void_p(out.ctypes.data), ctypes.c_void_p(ptr),
+                       ctypes.c_size_t(4 * n), ctypes.c_int(2))
+    assert rc == 0
+    return out
+
+
+def run_synth_gpu(torch, S, d, k, R, alpha, gamma, mu, flags, stream=None):
+    h = S.Sma(d, k, alpha, gamma, mu, sma_inputs.w0(d), flags=flags)
+    stream = stream or torch.cuda.Stream()   # non-default: CUDA-graph variants capture on it
+    for i in range(R):
+        h.synth_grads(i, sma_inputs.SEED_G, stream)
+        h.step(stream)
+    return h
+
+
+# ------------------------------------------------------------ exact traces
+@pytest.mark.parametrize("variant", list(COLLECTIVE_FLAGS))
+@pytest.mark.parametrize("k,alpha,gamma,mu", [
+    (2, 0.5, 0.25, 0.5),       # the north_star's hand-unrolled 2-replica, 4-parameter case
+    (4, 0.25, 0.125, 0.5),
+])
+def test_dyadic_trace_bitwise(torch_cuda, S, variant, k, alpha, gamma, mu):
+    """Dyadic inputs keep fp32 exact for the first rounds:
+    GPU == exact-rational brute force bit for bit, every variant."""
+    torch = torch_cuda
+    d, R = 4, 8
+    w0 = sma_inputs.dyadic(d, 100 + k)
+    G = sma_inputs.dyadic((R, k, d), 200 + k)
+    tr = exact.sma_exact(list(w0), G.tolist(), alpha, gamma, mu)
+    h = S.Sma(d, k, alpha, gamma, mu, w0.astype(np.float32), flags=COLLECTIVE_FLAGS[variant])
+    gd = torch.tensor(G, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    stream = torch.cuda.Stream()
+    for i in range(R):
+        for j in range(k):
+            h.set_grads(j, gd[i, j])
+        h.step(stream)
+        z, zp, W = tr[i + 1]
+        assert h.central().tolist() == [float(v) for v in z], (variant, i)
+        assert h.central_prev().tolist() == [float(v) for v in zp], (variant, i)
+        for j in range(k):
+            assert h.replica(j).tolist() == [float(v) for v in W[j]], (variant, i, j)
+    h.close()
+
+
+def test_synth_generator_bitwise(torch_cuda, S):
+    """synth_grads == the shared input module bit for bit: with w = 0, gamma = 1,
+    alpha = mu = 0 one round leaves w_j = -g_j exactly."""
+    d, k = 10_007, 3
+    h = S.Sma(d, k, 0.0, 1.0, 0.0, np.zeros(d, np.float32))
+    h.synth_grads(7, sma_inputs.SEED_G, torch_cuda.cuda.current_stream())
+    h.step(torch_cuda.cuda.current_stream())
+    for j in range(k):
+        assert np.array_equal(-h.replica(j), sma_inputs.grad(7, j, k, d))
+    h.close()
+
+
+def test_alpha_zero_is_fp32_sgd_bitwise(torch_cuda, S):
+    """alpha = 0: z stays w0 bitwise for any mu, and each replica
+    is bitwise an fp32 SGD loop (gamma = 2^-3 makes gamma*g exact, so the FMA
+    and the two-step form agree)."""
+    d, k, R = 5_003, 2, 20
+    gamma = 0.125
+    h = run_synth_gpu(torch_cuda, S, d, k, R, 0.0, gamma, 0.9, 0)
+    w = np.tile(sma_inputs.w0(d), (k, 1))
+    for i in range(R):
+        for j in range(k):
+            w[j] = (w[j] - np.float32(gamma) * sma_inputs.grad(i, j, k, d)).astype(np.float32)
+    assert np.array_equal(h.central(), sma_inputs.w0(d))
+    for j in range(k):
+        assert np.array_equal(h.replica(j), w[j])
+    h.close()
+
+
+# ------------------------------------------------------- 100-round parity
+@pytest.mark.parametrize("variant", list(COLLECTIVE_FLAGS))
+@pytest.mark.parametrize("d,k", [(100_003, 4), (4_097, 7)])
+def test_synth_100_rounds_parity(torch_cuda, S, variant, d, k):
+    """Several tiles and a ragged tail (d % 4 != 0), 100 rounds, every variant."""
+    R = 100
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    h = run_synth_gpu(torch_cuda, S, d, k, R, a, g, m, COLLECTIVE_FLAGS[variant])
+    zr, zpr, Wr = pytest.importorskip("oracle").run_synth(d, k, a, g, m, R, sma_inputs.SEED_W,
+                                                           sma_inputs.SEED_G)
+    assert relerr(h.central(), zr) <= TOL
+    assert relerr(h.central_prev(), zpr) <= TOL
+    for j in range(k):
+        assert relerr(h.replica(j), Wr[j]) <= TOL
+    # padding [d, d_pad) stays exactly zero in every replica and in z
+    for j in range(k):
+        assert np.all(dev_read(S.sma_replica_device_ptr(h.h, j), h.d_pad)[d:] == 0)
+    assert np.all(dev_read(S.sma_central_device_ptr(h.h), h.d_pad)[d:] == 0)
+    h.close()
+
+
+def test_mode_b_with_distinct_initial_replicas(torch_cuda, S, orc):
+    """Mode B's prologue Q^0 = sum_j (w_j - z_prev) with distinct replicas (R3
+    alternative via sma_set_replica), and again after a mid-run set_central."""
+    d, k, R = 3_001, 4, 40
+    a, g, m = F32(0.25), F32(0.1), F32(0.9)
+    rng = np.random.default_rng(3)
+    w0 = sma_inputs.w0(d)
+    Winit = (w0 + rng.uniform(-0.05, 0.05, (k, d))).astype(np.float32)
+    stream = torch_cuda.cuda.Stream()
+    for flags in (0, 16, 16 | 1, 16 | 1 | 8):
+        h = S.Sma(d, k, a, g, m, w0, flags=flags)
+        for j in range(k):
+            h.set_replica(j, Winit[j])
+        st = orc.State.init(w0, k, Winit.astype(np.float64))
+        for i in range(R):
+            h.synth_grads(i, sma_inputs.SEED_G, stream)
+            h.step(stream)
+            st.round(np.stack([sma_inputs.grad(i, j, k, d) for j in range(k)]), a, g, m)
+            if i == R // 2:  # checkpoint round trip mid-run
+                z, zp = h.central(), h.central_prev()
+                h.set_central(z, zp)
+        assert relerr(h.central(), st.z) <= TOL, flags
+        for j in range(k):
+            assert relerr(h.replica(j), st.W[j]) <= TOL, flags
+        h.close()
+
+
+def test_learner_softmax_c1_parity(torch_cuda, S, orc):
+    """Config C1: softmax regression d = 7,850, k = 4, batch 16, 100 rounds on
+    MNIST-shaped blobs, built-in learner in the loop, vs the oracle."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(60_000, seed=4)
+    k, b, R = 4, 16, 100
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    w0 = np.zeros(7850, np.float32)
+    Xd = torch.from_numpy(X).cuda()
+    yd = torch.from_numpy(y).cuda()
+    for flags in (0, 16 | 1):
+        h = S.Sma(7850, k, a, g, m, w0, flags=flags)
+        S.sma_learner_attach(h.h, 0, 784, 0, 10, b, Xd, yd, X.shape[0], 99)
+        for i in range(R):
+            S.sma_learner_grads(h.h, i, torch.cuda.current_stream())
+            h.step()
+        zr, _, Wr = orc.run_softmax(X, y, b, 99, k, a, g, m, R, w0.astype(np.float64))
+        assert relerr(h.central(), zr) <= TOL
+        for j in range(k):
+            assert relerr(h.replica(j), Wr[j]) <= TOL
+        acc = np.mean(np.argmax(X @ h.central()[:7840].reshape(10, 784).T + h.central()[7840:], 1) == y)
+        assert acc > 0.99
+        h.close()
+
+
+def test_learner_gradient_single_round(torch_cuda, S, orc):
+    """One learner gradient at a random point (gamma = 1, alpha = mu = 0):
+    w_j' = w_j - g_j, compared with the fp64 gradient of the same batch."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(1_000, seed=8)
+    k, b = 3, 16
+    w0 = np.random.default_rng(1).normal(0, 0.01, 7850).astype(np.float32)
+    h = S.Sma(7850, k, 0.0, 1.0, 0.0, w0)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    S.sma_learner_attach(h.h, 0, 784, 0, 10, b, Xd, yd, X.shape[0], 5)
+    rnd = 70   # crosses into epoch 3 (E = 20)
+    S.sma_learner_grads(h.h, rnd, torch.cuda.current_stream())
+    h.step()
+    for j in range(k):
+        rows = orc.batch_indices(X.shape[0], k, b, 5, rnd, j)
+        _, gref = orc.softmax_loss_grad(X, y, rows, w0.astype(np.float64))
+        gpu = w0.astype(np.float64) - h.replica(j)
+        assert np.max(np.abs(gpu - gref)) < 2e-6
+    h.close()
+
+
+# -------------------------------------------------- full size (bench config)
+def test_c4_full_size_sampled_parity(torch_cuda, S, orc):
+    """BASELINE metric config at N = 1: ResNet-50 size d = 25,557,032, k = 16,
+    alpha = 1/16, gamma = 0.1, mu = 0.9, the launch configuration bench.py times
+    (fused kernel), 100 rounds with fresh synthetic gradients each round; the
+    oracle runs the identical computation on a sampled index set (separable per
+    index); padding checked exactly."""
+    d, k, R = sma_inputs.CONFIGS["C4"]["d"], 16, 100
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    h = run_synth_gpu(torch_cuda, S, d, k, R, a, g, m, 0)
+    idx = sma_inputs.sample_indices(d, h.d_pad, 1, [0, h.d_pad], n_random=65_536)
+    zr, zpr, Wr = orc.run_synth(d, k, a, g, m, R, sma_inputs.SEED_W, sma_inputs.SEED_G, idx)
+    z = h.central()
+    assert relerr(z[idx], zr) <= TOL
+    assert relerr(h.central_prev()[idx], zpr) <= TOL
+    for j in range(k):
+        assert relerr(h.replica(j)[idx], Wr[j]) <= TOL
+    h.close()
+
+
+# ------------------------------------------------------------ API behaviour
+def test_errors_and_state(torch_cuda, S):
+    torch = torch_cuda
+    d, k = 1000, 2
+    h = S.Sma(d, k, 0.5, 0.1, 0.9, np.zeros(d, np.float32))
+    with pytest.raises(S.SmaError) as e:
+        h.step()
+    assert e.value.status == 3                                  # GRADS_MISSING
+    g = torch.zeros(d + 1, device="cuda")
+    with pytest.raises(S.SmaError) as e:
+        h.set_grads(0, g.data_ptr() + 4)                          # misaligned
+    assert e.value.status == 1
+    with pytest.raises(S.SmaError) as e:
+        h.set_grads(2, g)                                         # j out of range
+    assert e.value.status == 1
+    with pytest.raises(S.SmaError) as e:
+        S.sma_learner_grads(h.h, 0)                               # no learner attached
+    assert e.value.status == 8
+    h.close()
+
+
+def test_edge_sizes(torch_cuda, S, orc):
+    """d = 1 (all padding but one), k = 1, and the maximum r = 64 replicas."""
+    for d, k in [(1, 1), (1, 3), (5, 64), (515, 64)]:
+        a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+        h = run_synth_gpu(torch_cuda, S, d, k, 10, a, g, m, 0)
+        zr, _, Wr = orc.run_synth(d, k, a, g, m, 10, sma_inputs.SEED_W, sma_inputs.SEED_G)
+        assert relerr(h.central(), zr) <= TOL
+        assert relerr(h.replica(k - 1), Wr[k - 1]) <= TOL
+        h.close()
+    with pytest.raises(S.SmaError):
+        S.Sma(8, 65, 0.1, 0.1, 0.9, np.zeros(8, np.float32))
+
+
+def test_restart_and_hparams(torch_cuda, S, orc):
+    """SMA restart: replicas := z, z_prev := z; then rounds with new
+    hyper-parameters match the oracle started from that state."""
+    d, k = 2_049, 4
+    a, g, m = F32(0.25), F32(0.1), F32(0.9)
+    for flags in (0, 16 | 1):
+        h = run_synth_gpu(torch_cuda, S, d, k, 5, a, g, m, flags)
+        h.restart()
+        z = h.central().astype(np.float64)
+        for j in range(k):
+            assert np.array_equal(h.replica(j), h.central())
+        assert np.array_equal(h.central_prev(), h.central())
+        h.set_hparams(F32(0.2), F32(0.05), F32(0.5))
+        st = orc.State.init(z, k)
+        for i in range(5, 15):
+            h.synth_grads(i, sma_inputs.SEED_G)
+            h.step()
+            st.round(np.stack([sma_inputs.grad(i, j, k, d) for j in range(k)]),
+                     F32(0.2), F32(0.05), F32(0.5))
+        assert relerr(h.central(), st.z) <= TOL
+        h.close()
+
+
+def test_nonfinite_is_reported(torch_cuda, S):
+    torch = torch_cuda
+    d = 100
+    h = S.Sma(d, 2, 0.5, 0.1, 0.9, np.zeros(d, np.float32), flags=S.FLAG_CHECK_FINITE)
+    g = torch.zeros((2, d), device="cuda")
+    g[1, 17] = float("inf")
+    h.set_grads(0, g[0])
+    h.set_grads(1, g[1])
+    h.step()
+    with pytest.raises(S.SmaError) as e:
+        h.central()
+    assert e.value.status == 4
+    h.close()
+
+
+def test_host_gradient_path_and_timing(torch_cuda, S, orc):
+    """sma_set_learner_grads_host (the e2e path) and SMA_FLAG_TIMING."""
+    torch = torch_cuda
+    d, k, R = 9_999, 3, 6
+    a, g, m = F32(1 / 3), F32(0.1), F32(0.9)
+    h = S.Sma(d, k, a, g, m, sma_inputs.w0(d), flags=S.FLAG_TIMING)
+    pinned = [torch.empty(d, dtype=torch.float32).pin_memory() for _ in range(k)]
+    s = torch.cuda.current_stream()
+    for i in range(R):
+        s.synchronize()
+        for j in range(k):
+            pinned[j].copy_(torch.from_numpy(sma_inputs.grad(i, j, k, d)))
+            h.set_grads_host(j, pinned[j], s)
+        h.step(s)
+    zr, _, _ = orc.run_synth(d, k, a, g, m, R, sma_inputs.SEED_W, sma_inputs.SEED_G)
+    assert relerr(h.central(), zr) <= TOL
+    ms, n = h.kernel_time()
+    assert n == R and ms > 0
+    h.close()
