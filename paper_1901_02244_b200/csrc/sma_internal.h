@@ -35,11 +35,17 @@ struct ReplicaArgs {
   float* C;            // MATERIALIZE_C: c_j buffer [r][ld] (else nullptr)
   float alpha, gamma, mu;
   int* nonfinite;      // CHECK_FINITE flag or nullptr
+  int64_t c0;          // first float4 chunk this launch covers (LDG tail after TMA)
 };
 
 // Launchers (return the launch error, never synchronise).
 cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a, int num_sms,
                                 cudaStream_t s);
+// TMA variant internals (sma_kernels_tma.cu): full kTile tiles below d.
+int64_t tma_full_tiles(int64_t d);
+int64_t tma_tile_floats();
+cudaError_t launch_replica_step_tma(int mode, const ReplicaArgs& a, int64_t ntiles, int num_sms,
+                                    cudaStream_t s);
 // MATERIALIZE_C second pass: reduce C over replicas (warp shuffle + block tree),
 // then the fused z update (mode kFused) or the partial (kPartialA).
 cudaError_t launch_reduce_corrections(int mode, const ReplicaArgs& a, int num_sms,

@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads, 4) replica_step_ldg(const ReplicaArg
   const int64_t dfull4 = a.d >> 2;  // chunks entirely below d: vector path
   const bool matc = a.C != nullptr;
   bool bad = false;
-  for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < dfull4; c += stride) {
+  for (int64_t c = a.c0 + (int64_t)blockIdx.x * kThreads + threadIdx.x; c < dfull4; c += stride) {
     const int64_t p0 = c << 2;
     const float4 z = ld_ro(a.z + p0);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -151,7 +151,8 @@ __global__ void __launch_bounds__(kThreads, 4) replica_step_ldg(const ReplicaArg
   }
   // The chunk straddling d and the zero padding [d, d_pad): gradients are read
   // with scalar loads below d and taken as 0 above it (padding stays 0).
-  for (int64_t c = dfull4 + (int64_t)blockIdx.x * kThreads + threadIdx.x; c < a.n4; c += stride) {
+  const int64_t tail0 = dfull4 > a.c0 ? dfull4 : a.c0;
+  for (int64_t c = tail0 + (int64_t)blockIdx.x * kThreads + threadIdx.x; c < a.n4; c += stride) {
     const int64_t p0 = c << 2;
     const float4 z = ld_ro(a.z + p0);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -408,23 +409,32 @@ int grid_for(K kernel, int threads, size_t smem, int64_t work_items, int num_sms
 }  // namespace
 
 // ----------------------------------------------------------------- launchers
-cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a, int num_sms,
+cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int num_sms,
                                 cudaStream_t s) {
-  if (tma) return cudaErrorNotSupported;  // TMA variant: see sma_kernels_tma.cu
+  ReplicaArgs a = a0;
+  a.c0 = 0;
+  if (tma) {  // TMA-staged full tiles, then the LDG kernel for the rest
+    const int64_t nt = tma_full_tiles(a.d);
+    cudaError_t e = launch_replica_step_tma(mode, a, nt, num_sms, s);
+    if (e != cudaSuccess) return e;
+    a.c0 = nt * tma_tile_floats() / 4;
+    if (a.c0 >= a.n4) return cudaSuccess;
+  }
+  const int64_t work = a.n4 - a.c0;
   switch (mode) {
     case kFused: {
       auto k = replica_step_ldg<kFused>;
-      k<<<grid_for(k, kThreads, 0, a.n4, num_sms), kThreads, 0, s>>>(a);
+      k<<<grid_for(k, kThreads, 0, work, num_sms), kThreads, 0, s>>>(a);
       break;
     }
     case kPartialA: {
       auto k = replica_step_ldg<kPartialA>;
-      k<<<grid_for(k, kThreads, 0, a.n4, num_sms), kThreads, 0, s>>>(a);
+      k<<<grid_for(k, kThreads, 0, work, num_sms), kThreads, 0, s>>>(a);
       break;
     }
     case kPartialB: {
       auto k = replica_step_ldg<kPartialB>;
-      k<<<grid_for(k, kThreads, 0, a.n4, num_sms), kThreads, 0, s>>>(a);
+      k<<<grid_for(k, kThreads, 0, work, num_sms), kThreads, 0, s>>>(a);
       break;
     }
     default: return cudaErrorInvalidValue;

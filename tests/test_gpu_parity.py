@@ -44,6 +44,10 @@ COLLECTIVE_FLAGS = {
     "collA_matc": 16 | 2,
     "collB": 16 | 1,
     "collB_graph": 16 | 1 | 8,
+    "fused_tma": 64,
+    "matc_tma": 2 | 64,
+    "collA_tma": 16 | 64,
+    "collB_tma_graph": 16 | 1 | 8 | 64,
 }
 
 
