@@ -52,7 +52,8 @@ def parse():
     ap.add_argument("--k", type=int, default=None, help="override total replicas")
     ap.add_argument("--mode", choices=["auto", "A", "B"], default="auto",
                     help="collective path mode when N > 1 (auto = B, the overlapped round)")
-    ap.add_argument("--tma", action="store_true", help="TMA-staged replica kernel variant")
+    ap.add_argument("--tma", action="store_true", help="force the TMA-staged replica kernel")
+    ap.add_argument("--ldg", action="store_true", help="force the direct-load replica kernel")
     ap.add_argument("--matc", action="store_true", help="north_star-literal c_j materialisation")
     ap.add_argument("--force-collective", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=10)
@@ -119,7 +120,7 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def cpu_baseline(d, k, alpha, gamma, mu, n_idx=1 << 23, rounds=3):
+def cpu_baseline(d, k, alpha, gamma, mu, n_idx=1 << 23, rounds=10):
     """The oracle as it stands (single thread, fp64), on a bounded sample of
     the same workload: all k replicas, `rounds` rounds, n_idx seeded parameter
     indices (SMA with given gradients is separable per index, so the sample
@@ -219,6 +220,9 @@ def main():
             flags |= sma.FLAG_OVERLAP
     if args.tma:
         flags |= sma.FLAG_KERNEL_TMA
+    if args.ldg:
+        flags |= sma.FLAG_KERNEL_LDG
+    use_tma = args.tma or (not args.ldg and not collective)   # libsma's default policy
     if args.matc:
         flags |= sma.FLAG_MATERIALIZE_C
 
@@ -264,19 +268,22 @@ def main():
     ms = ev0.elapsed_time(ev1)
     launches = h.launch_count() - l0
     clk = clocks.stop()
-    kern_ms, kern_n = h.kernel_time(reset=True)
+    phase_avg = []
+    for ph in range(4):   # replica kernel, reduce-scatter, shard update, all-gather
+        pm, pn = h.kernel_time(reset=True, phase=ph)
+        phase_avg.append(pm / pn if pn else 0.0)
 
-    t = torch.tensor([ms, kern_ms / max(kern_n, 1), float(launches)], dtype=torch.float64,
-                     device="cuda")
+    t = torch.tensor([ms, *phase_avg, float(launches)], dtype=torch.float64, device="cuda")
     if world > 1:
         tmax = t.clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         tsum = t.clone()
         dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        ms_max, kern_avg = float(tmax[0]), float(tmax[1])
-        launches_total = int(tsum[2])
+        ms_max, phase_avg = float(tmax[0]), [float(x) for x in tmax[1:5]]
+        launches_total = int(tsum[5])
     else:
-        ms_max, kern_avg, launches_total = ms, kern_ms / max(kern_n, 1), launches
+        ms_max, launches_total = ms, launches
+    kern_avg = phase_avg[0]
 
     # ------------------------------------------------------------------ e2e
     e2e = None
@@ -310,17 +317,18 @@ def main():
     if rank == 0:
         d_pad = h.d_pad
         peak, peak_src = measured_peaks()
+        kvar = "tma" if use_tma else "ldg"
         if mode == "fused":
             alg_bytes = 4 * d_pad * (3 * r + 3)
-            kname = "replica_step_ldg<kFused>"
+            kname = f"replica_step_{kvar}<kFused>"
         else:
             alg_bytes = 4 * d_pad * (3 * r + 2)
-            kname = "replica_step_ldg<kPartial%s>" % mode
+            kname = f"replica_step_{kvar}<kPartial{mode}>"
         if args.matc:
             alg_bytes = 4 * d_pad * (6 * r + (3 if mode == "fused" else 2))
         achieved = alg_bytes / (kern_avg * 1e-3) / 1e9
         traffic = None
-        tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_n{world}_{mode}.json")
+        tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_n{world}_{mode}_{kvar}.json")
         if os.path.exists(tpath):
             try:
                 traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
@@ -334,7 +342,7 @@ def main():
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_name(args.config, d, k), "d": d, "d_pad": d_pad,
                        "k": k, "replicas_per_gpu": r, "alpha": alpha, "gamma": gamma, "mu": mu,
-                       "mode": mode, "kernel": "tma" if args.tma else "ldg",
+                       "mode": mode, "kernel": kvar,
                        "materialize_c": bool(args.matc),
                        "parallelism": f"sma-dp{world}" + ("" if world == 1 else "+nccl-rs/ag"),
                        "l2": "no flush: per-round working set "
@@ -346,13 +354,21 @@ def main():
             "gpu_launches": launches_total,
             "clocks": clk,
         }
-        if world > 1:
-            link = 2 * 4 * d_pad * (world - 1) / world
-            line["nvlink"] = {"link_bytes_per_gpu_per_round": link,
-                              "note": "RS+AG bytes per GPU per round (nccl-tests bus "
-                                      "convention); overlapped with the replica kernel in Mode B",
-                              "bus_gbs_if_serial": link / (ms_max / args.steps * 1e-3) / 1e9,
-                              "peak_gbs": NVLINK_PEAK_GBS}
+        if collective:
+            one = 4 * d_pad * (world - 1) / world      # bus bytes of one RS (or AG) per GPU
+            rs_ms, up_ms, ag_ms = phase_avg[1], phase_avg[2], phase_avg[3]
+            bus = lambda ms_: (one / (ms_ * 1e-3) / 1e9) if ms_ > 0 else None  # noqa: E731
+            comb = (2 * one / ((rs_ms + ag_ms) * 1e-3) / 1e9) if rs_ms + ag_ms > 0 else None
+            line["nvlink"] = {
+                "bus_bytes_per_gpu_per_round": 2 * one,
+                "reduce_scatter_ms": rs_ms, "shard_update_ms": up_ms, "all_gather_ms": ag_ms,
+                "rs_bus_gbs": bus(rs_ms), "ag_bus_gbs": bus(ag_ms), "bus_gbs": comb,
+                "peak_gbs": NVLINK_PEAK_GBS,
+                "frac": (comb / NVLINK_PEAK_GBS) if comb else None,
+                "note": "nccl-tests bus convention busBW = 4 d_pad (n-1)/n / t per collective; "
+                        "times from CUDA events around each NCCL call on its stream, max over "
+                        "ranks" + ("; in Mode B they run concurrently with the replica kernel"
+                                   if mode == "B" else "")}
         if e2e:
             line["e2e"] = e2e
         if not args.no_cpu_baseline:

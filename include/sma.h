@@ -89,8 +89,12 @@ enum {
      * (sma_kernel_time). */
     SMA_FLAG_TIMING = 32u,
     /* Replica kernel variant: TMA bulk-copy (cp.async.bulk) shared-memory
-     * staging with an mbarrier pipeline instead of direct 128-bit loads. */
-    SMA_FLAG_KERNEL_TMA = 64u
+     * staging with an mbarrier pipeline (replica_step_tma) ... */
+    SMA_FLAG_KERNEL_TMA = 64u,
+    /* ... or direct 128-bit loads (replica_step_ldg).  With neither flag the
+     * library picks the faster one measured on B200: TMA for the
+     * fused n = 1 round, LDG on the collective path. */
+    SMA_FLAG_KERNEL_LDG = 128u
 };
 
 typedef struct {
@@ -255,9 +259,18 @@ sma_status sma_plan_batch_indices(int64_t n_samples, int32_t k, int32_t batch,
  * broadcast the bytes to the other ranks).  Errors: NCCL. */
 sma_status sma_nccl_unique_id(void* out);
 
-/* With SMA_FLAG_TIMING: total device milliseconds and number of replica-
- * kernel launches measured since the last reset (synchronises). */
-sma_status sma_kernel_time(sma_handle* h, double* total_ms, int64_t* launches, int reset);
+/* With SMA_FLAG_TIMING: total device milliseconds and number of timed
+ * intervals of `phase` since its last reset (synchronises).  Each interval is
+ * bracketed by CUDA events on the stream the phase runs on:
+ *   SMA_PHASE_REPLICA        the replica kernel launch(es) of a round (a3-a5[,a7])
+ *   SMA_PHASE_REDUCE_SCATTER ncclReduceScatter of the per-GPU partial (a6)
+ *   SMA_PHASE_SHARD_UPDATE   the shard update kernel (a7, collective path)
+ *   SMA_PHASE_ALL_GATHER     ncclAllGather of z (a8)
+ * Errors: INVALID_ARG (phase out of range). */
+enum { SMA_PHASE_REPLICA = 0, SMA_PHASE_REDUCE_SCATTER = 1, SMA_PHASE_SHARD_UPDATE = 2,
+       SMA_PHASE_ALL_GATHER = 3, SMA_NUM_PHASES = 4 };
+sma_status sma_kernel_time(sma_handle* h, int32_t phase, double* total_ms, int64_t* launches,
+                           int reset);
 
 /* Number of libsma CUDA kernels this handle has launched (NCCL collectives not counted). */
 int64_t sma_launch_count(const sma_handle* h);

@@ -172,22 +172,28 @@ __global__ void __launch_bounds__(kThreads, 4) replica_step_ldg(const ReplicaArg
 }
 
 // ---------------------------------------- MATERIALIZE_C: reduce c_j over j
-// The north_star-literal intra-GPU reduction: a warp covers 8 float4 columns
-// x 4 replica groups (lane = group*8 + column); each lane sums its replicas
-// j = group + 4*warp + 32*t, the 4 groups are combined with two xor-shuffles,
-// and the 8 warps of the block with a shared-memory tree.
+// The north_star-literal intra-GPU reduction of the materialised corrections.
+// A warp covers 8 float4 columns x 4 replica groups (lane = group*8 + column:
+// four 128-byte row segments per load); the 8 warps of a block form
+// `wc` column sets x `wr` replica slices (wr*wc = 8, wr = min(8, ceil(r/4))
+// rounded up to a power of two).  Lane (group g, slice s) sums replicas
+// j = g + 4 (s + wr t); the 4 groups are combined with two xor-shuffles and
+// the wr slices with a shared-memory tree.
 constexpr int kRedWarps = 8;
 template <int MODE>
-__global__ void __launch_bounds__(kRedWarps * 32) reduce_corrections(const ReplicaArgs a) {
+__global__ void __launch_bounds__(kRedWarps * 32) reduce_corrections(const ReplicaArgs a, int wr) {
   __shared__ float4 part[kRedWarps][8];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int col = lane & 7, grp = lane >> 3;
-  const int64_t ntiles = (a.n4 + 7) / 8;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t c = t * 8 + col;
+  const int wc = kRedWarps / wr;
+  const int cs = warp % wc, sl = warp / wc;     // column set, replica slice
+  const int64_t cols_per_block = 8 * wc;
+  const int64_t nblk = (a.n4 + cols_per_block - 1) / cols_per_block;
+  for (int64_t t = blockIdx.x; t < nblk; t += gridDim.x) {
+    const int64_t c = t * cols_per_block + cs * 8 + col;
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
     if (c < a.n4) {
-      for (int j = grp + 4 * warp; j < a.r; j += 4 * kRedWarps) {
+      for (int j = grp + 4 * sl; j < a.r; j += 4 * wr) {
         const float4 v = ld_ro(a.C + (int64_t)j * a.ld + (c << 2));
         s.x = __fadd_rn(s.x, v.x); s.y = __fadd_rn(s.y, v.y);
         s.z = __fadd_rn(s.z, v.z); s.w = __fadd_rn(s.w, v.w);
@@ -202,19 +208,19 @@ __global__ void __launch_bounds__(kRedWarps * 32) reduce_corrections(const Repli
     }
     if (grp == 0) part[warp][col] = s;
     __syncthreads();
-#pragma unroll
-    for (int h = kRedWarps / 2; h >= 1; h >>= 1) {  // block-level tree over warps
-      if (warp < h && grp == 0) {
-        float4 o = part[warp + h][col], m = part[warp][col];
+    for (int h = wr / 2; h >= 1; h >>= 1) {  // block-level tree over replica slices
+      if (sl < h && grp == 0) {
+        const float4 o = part[warp + h * wc][col];
+        float4 m = part[warp][col];
         m.x = __fadd_rn(m.x, o.x); m.y = __fadd_rn(m.y, o.y);
         m.z = __fadd_rn(m.z, o.z); m.w = __fadd_rn(m.w, o.w);
         part[warp][col] = m;
       }
       __syncthreads();
     }
-    if (warp == 0 && grp == 0 && c < a.n4) {
+    if (sl == 0 && grp == 0 && c < a.n4) {
       const int64_t p0 = c << 2;
-      const float4 acc = part[0][col];
+      const float4 acc = part[warp][col];
       if (MODE == kFused) {
         const float4 z = ld_ro(a.z + p0);
         const float4 zp = ld_rw(a.zprev_next + p0);
@@ -444,13 +450,16 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
 
 cudaError_t launch_reduce_corrections(int mode, const ReplicaArgs& a, int num_sms,
                                       cudaStream_t s) {
-  const int64_t tiles = (a.n4 + 7) / 8;
+  int wr = 1;
+  while (wr < kRedWarps && 4 * wr < a.r) wr <<= 1;
+  const int64_t cols = 8 * (kRedWarps / wr);
+  const int64_t blocks = (a.n4 + cols - 1) / cols;
   const int64_t cap = (int64_t)num_sms * 8;
-  const int grid = (int)(tiles < cap ? tiles : cap);
+  const int grid = (int)(blocks < cap ? blocks : cap);
   if (mode == kFused)
-    reduce_corrections<kFused><<<grid, kRedWarps * 32, 0, s>>>(a);
+    reduce_corrections<kFused><<<grid, kRedWarps * 32, 0, s>>>(a, wr);
   else if (mode == kPartialA)
-    reduce_corrections<kPartialA><<<grid, kRedWarps * 32, 0, s>>>(a);
+    reduce_corrections<kPartialA><<<grid, kRedWarps * 32, 0, s>>>(a, wr);
   else
     return cudaErrorInvalidValue;
   return cudaGetLastError();

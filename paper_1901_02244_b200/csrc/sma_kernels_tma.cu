@@ -10,26 +10,28 @@
 // Tiles that straddle d and the padding are left to the LDG kernel (tail launch).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "sma_internal.h"
 
 namespace sma {
 namespace {
 
-constexpr int kTile = 2048;                 // floats per stream per tile (8 KB)
-constexpr int kStages = 8;                  // (w, g) slots in flight: 8 x 16 KB
+// Tile (floats per stream per TMA op) and ring depth; the default
+// (2048 floats = 8 KB, 8 stages = 128 KB of (w, g) in flight per SM) was the
+// best of the sweep in profiles/r01_sweep_tma.jsonl.  SMA_TMA_CONFIG=<i>
+// selects another entry of kTmaConfigs (tuning knob, documented in DESIGN.md).
 constexpr int kConsumerWarps = 8;
 constexpr int kConsumers = kConsumerWarps * 32;
 constexpr int kThreadsTma = kConsumers + 32;  // + 1 producer warp
-constexpr int kVecPerThread = kTile / 4 / kConsumers;  // float4s per consumer thread (2)
-static_assert(kTile % (4 * kConsumers) == 0, "tile must split evenly");
 
+template <int TILE, int STAGES>
 struct __align__(128) TmaSmem {
-  float w[kStages][kTile];
-  float g[kStages][kTile];
-  float z[2][kTile];
-  float zp[2][kTile];
-  uint64_t full[kStages], empty[kStages];
+  float w[STAGES][TILE];
+  float g[STAGES][TILE];
+  float z[2][TILE];
+  float zp[2][TILE];
+  uint64_t full[STAGES], empty[STAGES];
   uint64_t zfull[2], zempty[2];
 };
 
@@ -91,11 +93,14 @@ __device__ __forceinline__ float central(float z, float s, float zp, float mu) {
   return __fadd_rn(__fadd_rn(z, s), __fmul_rn(mu, __fsub_rn(z, zp)));
 }
 
-template <int MODE>
+template <int MODE, int TILE, int STAGES>
 __global__ void __launch_bounds__(kThreadsTma, 1)
     replica_step_tma(const ReplicaArgs a, int64_t ntiles) {
+  constexpr int kTile = TILE, kStages = STAGES;
+  constexpr int kVecPerThread = kTile / 4 / kConsumers;  // float4s per consumer thread
+  static_assert(kTile % (4 * kConsumers) == 0, "tile must split evenly");
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  TmaSmem& sm = *reinterpret_cast<TmaSmem*>(smem_raw);
+  TmaSmem<TILE, STAGES>& sm = *reinterpret_cast<TmaSmem<TILE, STAGES>*>(smem_raw);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool need_zp = (MODE == kFused);
   if (threadIdx.x == 0) {
@@ -210,29 +215,62 @@ __global__ void __launch_bounds__(kThreadsTma, 1)
   if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
 }
 
-template <int MODE>
+template <int MODE, int TILE, int STAGES>
 cudaError_t launch_mode(const ReplicaArgs& a, int64_t ntiles, int num_sms, cudaStream_t s) {
-  auto k = replica_step_tma<MODE>;
-  const int smem = (int)sizeof(TmaSmem);
+  auto k = replica_step_tma<MODE, TILE, STAGES>;
+  const int smem = (int)sizeof(TmaSmem<TILE, STAGES>);
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;
-  const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
+  int occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreadsTma, smem) != cudaSuccess ||
+      occ < 1)
+    occ = 1;
+  const int64_t cap = (int64_t)num_sms * occ;
+  const int grid = (int)(ntiles < cap ? ntiles : cap);
   k<<<grid, kThreadsTma, smem, s>>>(a, ntiles);
   return cudaGetLastError();
 }
 
+struct TmaConfig { int tile, stages; };
+// index 0 is the default
+constexpr TmaConfig kTmaConfigs[] = {{2048, 8}, {4096, 4}, {1024, 16}, {2048, 4}, {1024, 6},
+                                     {4096, 2}, {2048, 12}};
+constexpr int kNumTmaConfigs = sizeof(kTmaConfigs) / sizeof(kTmaConfigs[0]);
+
+int tma_config() {
+  static int cfg = [] {
+    const char* e = getenv("SMA_TMA_CONFIG");
+    int v = e ? atoi(e) : 0;
+    return (v >= 0 && v < kNumTmaConfigs) ? v : 0;
+  }();
+  return cfg;
+}
+
+template <int MODE>
+cudaError_t launch_cfg(const ReplicaArgs& a, int64_t ntiles, int num_sms, cudaStream_t s) {
+  switch (tma_config()) {
+    case 1: return launch_mode<MODE, 4096, 4>(a, ntiles, num_sms, s);
+    case 2: return launch_mode<MODE, 1024, 16>(a, ntiles, num_sms, s);
+    case 3: return launch_mode<MODE, 2048, 4>(a, ntiles, num_sms, s);
+    case 4: return launch_mode<MODE, 1024, 6>(a, ntiles, num_sms, s);
+    case 5: return launch_mode<MODE, 4096, 2>(a, ntiles, num_sms, s);
+    case 6: return launch_mode<MODE, 2048, 12>(a, ntiles, num_sms, s);
+    default: return launch_mode<MODE, 2048, 8>(a, ntiles, num_sms, s);
+  }
+}
+
 }  // namespace
 
-int64_t tma_full_tiles(int64_t d) { return d / kTile; }
-int64_t tma_tile_floats() { return kTile; }
+int64_t tma_tile_floats() { return kTmaConfigs[tma_config()].tile; }
+int64_t tma_full_tiles(int64_t d) { return d / tma_tile_floats(); }
 
 cudaError_t launch_replica_step_tma(int mode, const ReplicaArgs& a, int64_t ntiles, int num_sms,
                                     cudaStream_t s) {
   if (ntiles <= 0) return cudaSuccess;
   switch (mode) {
-    case kFused: return launch_mode<kFused>(a, ntiles, num_sms, s);
-    case kPartialA: return launch_mode<kPartialA>(a, ntiles, num_sms, s);
-    case kPartialB: return launch_mode<kPartialB>(a, ntiles, num_sms, s);
+    case kFused: return launch_cfg<kFused>(a, ntiles, num_sms, s);
+    case kPartialA: return launch_cfg<kPartialA>(a, ntiles, num_sms, s);
+    case kPartialB: return launch_cfg<kPartialB>(a, ntiles, num_sms, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -221,8 +221,9 @@ struct sma_handle {
   cudaGraphExec_t gexec[2] = {nullptr, nullptr};
   uint64_t gver[2] = {0, 0};
 
-  std::vector<cudaEvent_t> tev;  // (start, stop) pairs
-  size_t tused = 0;
+  // SMA_FLAG_TIMING: (start, stop) event pairs per phase (SMA_PHASE_*)
+  std::vector<cudaEvent_t> tev[SMA_NUM_PHASES];
+  size_t tused[SMA_NUM_PHASES] = {};
   int64_t launches = 0;
 
   // learner
@@ -270,7 +271,8 @@ void free_all(sma_handle* h) {
   for (int i = 0; i < 2; ++i)
     if (h->gexec[i]) cudaGraphExecDestroy(h->gexec[i]);
   if (h->comm) g_nccl.CommDestroy(h->comm);
-  for (cudaEvent_t e : h->tev) cudaEventDestroy(e);
+  for (auto& v : h->tev)
+    for (cudaEvent_t e : v) cudaEventDestroy(e);
   if (h->evFork) cudaEventDestroy(h->evFork);
   if (h->evJoin) cudaEventDestroy(h->evJoin);
   if (h->evDone) cudaEventDestroy(h->evDone);
@@ -323,6 +325,22 @@ sma_status check_nonfinite(sma_handle* h) {
   return SMA_OK;
 }
 
+// Next (start, stop) event pair of `phase` (nullptr unless SMA_FLAG_TIMING).
+sma_status timer_pair(sma_handle* h, int phase, cudaEvent_t** out) {
+  *out = nullptr;
+  if (!h->timing) return SMA_OK;
+  auto& v = h->tev[phase];
+  size_t& used = h->tused[phase];
+  while (used + 2 > v.size()) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreate(&e));
+    v.push_back(e);
+  }
+  *out = &v[used];
+  used += 2;
+  return SMA_OK;
+}
+
 sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s) {
   ReplicaArgs a{};
   a.W = h->W;
@@ -339,20 +357,9 @@ sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s) {
   a.gamma = h->gamma;
   a.mu = h->mu;
   a.nonfinite = h->check ? h->nonfinite : nullptr;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (h->timing) {
-    if (h->tused + 2 > h->tev.size()) {
-      for (int i = 0; i < 2; ++i) {
-        cudaEvent_t e;
-        CUDA_TRY(cudaEventCreate(&e));
-        h->tev.push_back(e);
-      }
-    }
-    e0 = h->tev[h->tused];
-    e1 = h->tev[h->tused + 1];
-    h->tused += 2;
-    CUDA_TRY(cudaEventRecord(e0, s));
-  }
+  cudaEvent_t* tp = nullptr;
+  STATUS_TRY(timer_pair(h, SMA_PHASE_REPLICA, &tp));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
   if (h->r > 0) {
     CUDA_TRY(launch_replica_step(mode, h->tma, a, h->num_sms, s));
     ++h->launches;
@@ -365,22 +372,41 @@ sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s) {
   } else {
     CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * h->d_pad, s));
   }
-  if (h->timing) CUDA_TRY(cudaEventRecord(e1, s));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
+  return SMA_OK;
+}
+
+// a6-a8 on stream s: reduce-scatter the per-GPU partial, update this GPU's
+// shard of z in place into the z_prev half, all-gather z.  Each phase is
+// bracketed by timing events with SMA_FLAG_TIMING.
+sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float coef_b,
+                         cudaStream_t s) {
+  const size_t cnt = (size_t)h->shard_len;
+  cudaEvent_t* tp = nullptr;
+  STATUS_TRY(timer_pair(h, SMA_PHASE_REDUCE_SCATTER, &tp));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
+  NCCL_TRY(g_nccl.ReduceScatter(partial, h->S, cnt, ncclFloat32, ncclSum, h->comm, s));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
+  STATUS_TRY(timer_pair(h, SMA_PHASE_SHARD_UPDATE, &tp));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
+  CUDA_TRY(launch_zsync(mode, h->S, h->z() + h->shard_off, h->zprev() + h->shard_off,
+                        h->shard_len / 4, h->alpha, h->mu, coef_b,
+                        h->check ? h->nonfinite : nullptr, h->num_sms, s));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
+  STATUS_TRY(timer_pair(h, SMA_PHASE_ALL_GATHER, &tp));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
+  NCCL_TRY(g_nccl.AllGather(h->zprev() + h->shard_off, h->zprev(), cnt, ncclFloat32, h->comm, s));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
   return SMA_OK;
 }
 
 // The body of one round, enqueued on stream s (capturable).
 sma_status enqueue_round(sma_handle* h, cudaStream_t s) {
-  const size_t cnt = (size_t)h->shard_len;
   if (!h->collective) {  // n == 1: a3-a7 fused in one kernel
     STATUS_TRY(replica_launch(h, kFused, nullptr, s));
   } else if (!h->overlap) {  // Mode A: paper order (fig:dependencies d/e)
     STATUS_TRY(replica_launch(h, kPartialA, h->P, s));
-    NCCL_TRY(g_nccl.ReduceScatter(h->P, h->S, cnt, ncclFloat32, ncclSum, h->comm, s));
-    CUDA_TRY(launch_zsync(kPartialA, h->S, h->z() + h->shard_off, h->zprev() + h->shard_off,
-                          h->shard_len / 4, h->alpha, h->mu, 0.f,
-                          h->check ? h->nonfinite : nullptr, h->num_sms, s));
-    NCCL_TRY(g_nccl.AllGather(h->zprev() + h->shard_off, h->zprev(), cnt, ncclFloat32, h->comm, s));
+    STATUS_TRY(enqueue_zsync(h, kPartialA, h->P, 0.f, s));
     h->launches += 1;  // zsync (NCCL's own kernels are not counted)
   } else {  // Mode B: z-sync(i) on sB  ||  replica kernel(i) on s
     float* Qcur = h->Q + (int64_t)h->qi * h->d_pad;
@@ -388,12 +414,7 @@ sma_status enqueue_round(sma_handle* h, cudaStream_t s) {
     const float coef_b = h->mu - h->alpha * (float)h->cfg.k;
     CUDA_TRY(cudaEventRecord(h->evFork, s));
     CUDA_TRY(cudaStreamWaitEvent(h->sB, h->evFork, 0));
-    NCCL_TRY(g_nccl.ReduceScatter(Qcur, h->S, cnt, ncclFloat32, ncclSum, h->comm, h->sB));
-    CUDA_TRY(launch_zsync(kPartialB, h->S, h->z() + h->shard_off, h->zprev() + h->shard_off,
-                          h->shard_len / 4, h->alpha, h->mu, coef_b,
-                          h->check ? h->nonfinite : nullptr, h->num_sms, h->sB));
-    NCCL_TRY(g_nccl.AllGather(h->zprev() + h->shard_off, h->zprev(), cnt, ncclFloat32, h->comm,
-                              h->sB));
+    STATUS_TRY(enqueue_zsync(h, kPartialB, Qcur, coef_b, h->sB));
     CUDA_TRY(cudaEventRecord(h->evJoin, h->sB));
     STATUS_TRY(replica_launch(h, kPartialB, Qnext, s));
     CUDA_TRY(cudaStreamWaitEvent(s, h->evJoin, 0));
@@ -423,7 +444,9 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
   h->collective = cfg->world > 1 || (f & SMA_FLAG_FORCE_COLLECTIVE);
   h->overlap = h->collective && (f & SMA_FLAG_OVERLAP);
   h->matc = (f & SMA_FLAG_MATERIALIZE_C) != 0;
-  h->tma = (f & SMA_FLAG_KERNEL_TMA) != 0;
+  if ((f & SMA_FLAG_KERNEL_TMA) && (f & SMA_FLAG_KERNEL_LDG))
+    return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_KERNEL_TMA and SMA_FLAG_KERNEL_LDG are exclusive");
+  h->tma = (f & SMA_FLAG_KERNEL_TMA) || (!(f & SMA_FLAG_KERNEL_LDG) && !h->collective);
   h->timing = (f & SMA_FLAG_TIMING) != 0;
   h->graphs = (f & SMA_FLAG_CUDA_GRAPH) != 0 && !h->timing;
   h->check = (f & SMA_FLAG_CHECK_FINITE) != 0;
@@ -788,19 +811,22 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
   return mark_done(h, s);
 }
 
-sma_status sma_kernel_time(sma_handle* h, double* total_ms, int64_t* launches, int reset) {
+sma_status sma_kernel_time(sma_handle* h, int32_t phase, double* total_ms, int64_t* launches,
+                           int reset) {
   if (!h || !total_ms || !launches) return fail(SMA_ERR_INVALID_ARG, "NULL argument");
+  if (phase < 0 || phase >= SMA_NUM_PHASES) return fail(SMA_ERR_INVALID_ARG, "bad phase %d", phase);
   DeviceGuard guard(h->dev);
   STATUS_TRY(sync_handle(h));
   double tot = 0;
-  for (size_t i = 0; i + 1 < h->tused; i += 2) {
+  const auto& v = h->tev[phase];
+  for (size_t i = 0; i + 1 < h->tused[phase]; i += 2) {
     float ms = 0;
-    CUDA_TRY(cudaEventElapsedTime(&ms, h->tev[i], h->tev[i + 1]));
+    CUDA_TRY(cudaEventElapsedTime(&ms, v[i], v[i + 1]));
     tot += ms;
   }
   *total_ms = tot;
-  *launches = (int64_t)(h->tused / 2);
-  if (reset) h->tused = 0;
+  *launches = (int64_t)(h->tused[phase] / 2);
+  if (reset) h->tused[phase] = 0;
   return SMA_OK;
 }
 

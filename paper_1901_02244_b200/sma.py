@@ -23,6 +23,7 @@ FLAG_CUDA_GRAPH = 8
 FLAG_FORCE_COLLECTIVE = 16
 FLAG_TIMING = 32
 FLAG_KERNEL_TMA = 64
+FLAG_KERNEL_LDG = 128
 MAX_LOCAL_REPLICAS = 64
 NCCL_ID_BYTES = 128
 
@@ -91,7 +92,7 @@ def load():
         "sma_plan_shard_range": ([i64, i32, i32, C.POINTER(i64), C.POINTER(i64)], st),
         "sma_plan_batch_indices": ([i64, i32, i32, u64, i64, i32, P], st),
         "sma_nccl_unique_id": ([P], st),
-        "sma_kernel_time": ([P, C.POINTER(C.c_double), C.POINTER(i64), C.c_int], st),
+        "sma_kernel_time": ([P, i32, C.POINTER(C.c_double), C.POINTER(i64), C.c_int], st),
         "sma_launch_count": ([P], i64),
         "sma_info": ([P, C.POINTER(i64), C.POINTER(i32), C.POINTER(i32), C.POINTER(i64),
                       C.POINTER(i64)], st),
@@ -253,9 +254,13 @@ def sma_nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-def sma_kernel_time(h: int, reset: bool = False) -> tuple[float, int]:
+PHASE_REPLICA, PHASE_REDUCE_SCATTER, PHASE_SHARD_UPDATE, PHASE_ALL_GATHER = 0, 1, 2, 3
+
+
+def sma_kernel_time(h: int, phase: int = PHASE_REPLICA, reset: bool = False) -> tuple[float, int]:
     ms, n = C.c_double(), C.c_int64()
-    _check(load().sma_kernel_time(h, C.byref(ms), C.byref(n), int(reset)), "sma_kernel_time")
+    _check(load().sma_kernel_time(h, phase, C.byref(ms), C.byref(n), int(reset)),
+           "sma_kernel_time")
     return ms.value, n.value
 
 
@@ -359,8 +364,8 @@ class Sma:
     def set_hparams(self, alpha, gamma, mu):
         sma_set_hparams(self.h, alpha, gamma, mu)
 
-    def kernel_time(self, reset=False):
-        return sma_kernel_time(self.h, reset)
+    def kernel_time(self, reset=False, phase=PHASE_REPLICA):
+        return sma_kernel_time(self.h, phase, reset)
 
     def launch_count(self):
         return sma_launch_count(self.h)

@@ -10,12 +10,16 @@ from paper_1901_02244_b200 import sma
 d = int(os.environ.get("SWEEP_D", sma_inputs.CONFIGS["C4"]["d"]))
 steps = int(os.environ.get("SWEEP_STEPS", "300"))
 w0 = sma_inputs.w0(d)
-cases = [(16, 0), (16, sma.FLAG_KERNEL_TMA), (2, 0), (2, sma.FLAG_KERNEL_TMA),
-         (2, sma.FLAG_FORCE_COLLECTIVE), (2, sma.FLAG_FORCE_COLLECTIVE | sma.FLAG_KERNEL_TMA),
-         (2, sma.FLAG_FORCE_COLLECTIVE | sma.FLAG_OVERLAP),
-         (2, sma.FLAG_FORCE_COLLECTIVE | sma.FLAG_OVERLAP | sma.FLAG_KERNEL_TMA),
-         (4, 0), (4, sma.FLAG_KERNEL_TMA), (32, 0), (32, sma.FLAG_KERNEL_TMA),
-         (16, sma.FLAG_MATERIALIZE_C)]
+L, T = sma.FLAG_KERNEL_LDG, sma.FLAG_KERNEL_TMA
+if os.environ.get("SWEEP_TMA_ONLY"):
+    cases = [(16, T), (2, T), (32, T), (2, T | sma.FLAG_FORCE_COLLECTIVE)]
+else:
+    cases = [(16, L), (16, T), (2, L), (2, T),
+             (2, sma.FLAG_FORCE_COLLECTIVE), (2, sma.FLAG_FORCE_COLLECTIVE | T),
+             (2, sma.FLAG_FORCE_COLLECTIVE | sma.FLAG_OVERLAP),
+             (2, sma.FLAG_FORCE_COLLECTIVE | sma.FLAG_OVERLAP | T),
+             (4, L), (4, T), (32, L), (32, T), (16, sma.FLAG_MATERIALIZE_C),
+             (16, sma.FLAG_MATERIALIZE_C | L), (2, sma.FLAG_MATERIALIZE_C)]
 for k, flags in cases:
     h = sma.Sma(d, k, 1.0 / k, 0.1, 0.9, w0, flags=flags | sma.FLAG_TIMING)
     s = torch.cuda.Stream()
@@ -37,7 +41,7 @@ for k, flags in cases:
     nbytes = 4 * h.d_pad * (3 * k + (2 if coll else 3))
     if flags & sma.FLAG_MATERIALIZE_C:
         nbytes = 4 * h.d_pad * (6 * k + 3)
-    print(json.dumps({"k": k, "flags": flags, "ms_per_round": ms, "rounds_s": 1000 / ms,
+    print(json.dumps({"k": k, "flags": flags, "tma_cfg": os.environ.get("SMA_TMA_CONFIG", "0"), "ms_per_round": ms, "rounds_s": 1000 / ms,
                       "kernel_ms": kms, "kernel_GBs": nbytes / kms / 1e6,
                       "frac": nbytes / kms / 1e6 / 6552.6}), flush=True)
     h.close()

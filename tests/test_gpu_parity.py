@@ -37,6 +37,7 @@ def relerr(got, ref):
 
 COLLECTIVE_FLAGS = {
     "fused": 0,
+    "fused_ldg": 128,
     "fused_graph": 8,
     "matc": 2,
     "collA": 16,
