@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--ldg", action="store_true", help="force the direct-load replica kernel")
     ap.add_argument("--matc", action="store_true", help="north_star-literal c_j materialisation")
     ap.add_argument("--force-collective", action="store_true")
+    ap.add_argument("--zsync", choices=["nccl", "nvls"], default="nccl",
+                    help="inter-GPU z-sync: NCCL RS/AG (default) or the fused multicast kernel")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -225,6 +227,8 @@ def main():
     use_tma = args.tma or (not args.ldg and not collective)   # libsma's default policy
     if args.matc:
         flags |= sma.FLAG_MATERIALIZE_C
+    if args.zsync == "nvls" and collective:
+        flags |= sma.FLAG_NVLS_ZSYNC
 
     nccl_id = None
     if world > 1:
@@ -269,7 +273,7 @@ def main():
     launches = h.launch_count() - l0
     clk = clocks.stop()
     phase_avg = []
-    for ph in range(4):   # replica kernel, reduce-scatter, shard update, all-gather
+    for ph in range(5):   # replica kernel, reduce-scatter, shard update, all-gather, nvls
         pm, pn = h.kernel_time(reset=True, phase=ph)
         phase_avg.append(pm / pn if pn else 0.0)
 
@@ -279,8 +283,8 @@ def main():
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         tsum = t.clone()
         dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        ms_max, phase_avg = float(tmax[0]), [float(x) for x in tmax[1:5]]
-        launches_total = int(tsum[5])
+        ms_max, phase_avg = float(tmax[0]), [float(x) for x in tmax[1:6]]
+        launches_total = int(tsum[6])
     else:
         ms_max, launches_total = ms, launches
     kern_avg = phase_avg[0]
@@ -344,7 +348,8 @@ def main():
                        "k": k, "replicas_per_gpu": r, "alpha": alpha, "gamma": gamma, "mu": mu,
                        "mode": mode, "kernel": kvar,
                        "materialize_c": bool(args.matc),
-                       "parallelism": f"sma-dp{world}" + ("" if world == 1 else "+nccl-rs/ag"),
+                       "parallelism": f"sma-dp{world}" + ("" if not collective else
+                                                           f"+{args.zsync}-zsync"),
                        "l2": "no flush: per-round working set "
                              f"{(alg_bytes / 1e9):.2f} GB/GPU >> 126 MB L2"},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
@@ -356,12 +361,16 @@ def main():
         }
         if collective:
             one = 4 * d_pad * (world - 1) / world      # bus bytes of one RS (or AG) per GPU
-            rs_ms, up_ms, ag_ms = phase_avg[1], phase_avg[2], phase_avg[3]
+            rs_ms, up_ms, ag_ms, nv_ms = phase_avg[1], phase_avg[2], phase_avg[3], phase_avg[4]
             bus = lambda ms_: (one / (ms_ * 1e-3) / 1e9) if ms_ > 0 else None  # noqa: E731
             comb = (2 * one / ((rs_ms + ag_ms) * 1e-3) / 1e9) if rs_ms + ag_ms > 0 else None
+            if nv_ms > 0:   # fused multicast kernel: same bus-byte convention over its time
+                comb = 2 * one / (nv_ms * 1e-3) / 1e9
             line["nvlink"] = {
                 "bus_bytes_per_gpu_per_round": 2 * one,
+                "zsync": args.zsync,
                 "reduce_scatter_ms": rs_ms, "shard_update_ms": up_ms, "all_gather_ms": ag_ms,
+                "nvls_zsync_ms": nv_ms,
                 "rs_bus_gbs": bus(rs_ms), "ag_bus_gbs": bus(ag_ms), "bus_gbs": comb,
                 "peak_gbs": NVLINK_PEAK_GBS,
                 "frac": (comb / NVLINK_PEAK_GBS) if comb else None,

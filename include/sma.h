@@ -94,7 +94,13 @@ enum {
     /* ... or direct 128-bit loads (replica_step_ldg).  With neither flag the
      * library picks the faster one measured on B200: TMA for the
      * fused n = 1 round, LDG on the collective path. */
-    SMA_FLAG_KERNEL_LDG = 128u
+    SMA_FLAG_KERNEL_LDG = 128u,
+    /* NEXT-1: the inter-GPU z-sync (reduce-scatter + shard update + all-gather)
+     * as ONE kernel on NVSwitch multicast memory (multimem.ld_reduce /
+     * multimem.st), with device-side barriers, instead of NCCL RS/AG.  Needs a
+     * device with CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED; sma_create fails with
+     * SMA_ERR_CUDA otherwise.  Collective path only. */
+    SMA_FLAG_NVLS_ZSYNC = 256u
 };
 
 typedef struct {
@@ -266,9 +272,10 @@ sma_status sma_nccl_unique_id(void* out);
  *   SMA_PHASE_REDUCE_SCATTER ncclReduceScatter of the per-GPU partial (a6)
  *   SMA_PHASE_SHARD_UPDATE   the shard update kernel (a7, collective path)
  *   SMA_PHASE_ALL_GATHER     ncclAllGather of z (a8)
+ *   SMA_PHASE_NVLS_ZSYNC     the fused multicast z-sync kernel (a6-a8, SMA_FLAG_NVLS_ZSYNC)
  * Errors: INVALID_ARG (phase out of range). */
 enum { SMA_PHASE_REPLICA = 0, SMA_PHASE_REDUCE_SCATTER = 1, SMA_PHASE_SHARD_UPDATE = 2,
-       SMA_PHASE_ALL_GATHER = 3, SMA_NUM_PHASES = 4 };
+       SMA_PHASE_ALL_GATHER = 3, SMA_PHASE_NVLS_ZSYNC = 4, SMA_NUM_PHASES = 5 };
 sma_status sma_kernel_time(sma_handle* h, int32_t phase, double* total_ms, int64_t* launches,
                            int reset);
 

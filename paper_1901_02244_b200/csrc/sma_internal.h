@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
+#include <string>
+
 #include "../../include/sma.h"
 
 namespace sma {
@@ -68,5 +71,35 @@ cudaError_t launch_softmax_grad(const float* X, const int32_t* y, const int32_t*
 // Broadcast: dst rows [r][ld] := src [ld]   and   y := x   (restart / init).
 cudaError_t launch_broadcast_rows(float* dst, int64_t ld, int r, const float* src, int64_t n4,
                                   int num_sms, cudaStream_t s);
+
+// ---------------------------------------------------------------- NVLS z-sync
+// One physical allocation per rank bound to an NVSwitch multicast object
+// (sma_nvls.cu).  uc: this rank's unicast mapping; mcva: the multicast mapping.
+struct NvlsRegion {
+  unsigned long long mc = 0, phys = 0;  // CUmemGenericAllocationHandle
+  unsigned long long uc = 0, mcva = 0;  // CUdeviceptr
+  size_t size = 0;
+  int dev = 0;
+  bool have_mc = false, have_phys = false, uc_mapped = false, mc_mapped = false, bound = false;
+};
+struct NvlsArgs {
+  const float* part_mc;  // multicast view of this round's per-GPU partial (P or Q[qi])
+  float* znext_mc;       // multicast view of z[1-cur] (receives z^{i+1})
+  const float* z;        // local z[cur]
+  const float* zprev;    // local z[1-cur] (z_prev of this GPU's shard)
+  int64_t off4, len4;    // this GPU's shard in float4 chunks
+  float alpha, mu, coef_b;
+  unsigned* flag_uc;     // [0] barrier A, [1] barrier B (local view)
+  unsigned* flag_mc;     // same, multicast view
+  unsigned* expect;      // [2] device-side barrier targets (local memory)
+  unsigned* done_ctr;    // CTA arrival counter (local memory)
+  int n;                 // number of GPUs
+  int* nonfinite;
+};
+bool nvls_supported(int device, std::string* err);
+bool nvls_setup(NvlsRegion* R, int device, int rank, int world, size_t bytes, const std::string& key,
+                const std::function<bool(std::string*)>& barrier, std::string* err);
+void nvls_teardown(NvlsRegion* R);
+cudaError_t launch_zsync_nvls(int mode, const NvlsArgs& a, int num_ctas, cudaStream_t s);
 
 }  // namespace sma

@@ -15,7 +15,10 @@
 #include <stdint.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
+
+#include <unistd.h>
 
 #include <cmath>
 #include <string>
@@ -70,7 +73,14 @@ struct NcclApi {
                                 ncclComm_t, cudaStream_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  // optional (user-buffer registration; absent in old NCCLs)
+  ncclResult_t (*MemAlloc)(void**, size_t) = nullptr;
+  ncclResult_t (*MemFree)(void*) = nullptr;
+  ncclResult_t (*CommRegister)(const ncclComm_t, void*, size_t, void**) = nullptr;
+  ncclResult_t (*CommDeregister)(const ncclComm_t, void*) = nullptr;
 };
 NcclApi g_nccl;
 
@@ -95,8 +105,14 @@ bool nccl_load() {
   BIND(CommAbort, "ncclCommAbort");
   BIND(ReduceScatter, "ncclReduceScatter");
   BIND(AllGather, "ncclAllGather");
+  BIND(AllReduce, "ncclAllReduce");
   BIND(GetErrorString, "ncclGetErrorString");
 #undef BIND
+  g_nccl.MemAlloc = reinterpret_cast<decltype(g_nccl.MemAlloc)>(dlsym(h, "ncclMemAlloc"));
+  g_nccl.MemFree = reinterpret_cast<decltype(g_nccl.MemFree)>(dlsym(h, "ncclMemFree"));
+  g_nccl.CommRegister = reinterpret_cast<decltype(g_nccl.CommRegister)>(dlsym(h, "ncclCommRegister"));
+  g_nccl.CommDeregister =
+      reinterpret_cast<decltype(g_nccl.CommDeregister)>(dlsym(h, "ncclCommDeregister"));
   g_nccl.ok = true;
   return true;
 }
@@ -214,6 +230,14 @@ struct sma_handle {
   uint64_t ver = 1;  // bumps when anything baked into a graph changes
 
   ncclComm_t comm = nullptr;
+  // collective buffers from ncclMemAlloc (NVLS-capable) and their registrations
+  std::vector<void*> nccl_allocs, nccl_regs;
+  int sync_sms = 16;  // SMs left to the overlapped z-sync in Mode B (SMA_SYNC_SMS)
+  // NEXT-1 multicast z-sync
+  bool nvls = false;
+  NvlsRegion nv;
+  size_t nv_off_part = 0, nv_off_z = 0;
+  unsigned* nv_ctl = nullptr;  // [0..1] expect, [2] done counter (local memory)
   cudaStream_t sB = nullptr, sIO = nullptr;
   cudaEvent_t evFork = nullptr, evJoin = nullptr, evDone = nullptr;
   bool any_work = false;
@@ -270,6 +294,24 @@ void free_all(sma_handle* h) {
   if (h->any_work) cudaDeviceSynchronize();
   for (int i = 0; i < 2; ++i)
     if (h->gexec[i]) cudaGraphExecDestroy(h->gexec[i]);
+  if (h->nvls) nvls_teardown(&h->nv);
+  cudaFree(h->nv_ctl);
+  if (h->nvls) {  // these live in the NVLS region, not in cudaMalloc memory
+    h->zbuf = nullptr;
+    h->P = nullptr;
+    h->Q = nullptr;
+  }
+  if (h->comm) {
+    for (void* r : h->nccl_regs)
+      if (g_nccl.CommDeregister) g_nccl.CommDeregister(h->comm, r);
+  }
+  for (void* p : h->nccl_allocs) {
+    if (p == h->zbuf) h->zbuf = nullptr;
+    if (p == h->P) h->P = nullptr;
+    if (p == h->S) h->S = nullptr;
+    if (p == h->Q) h->Q = nullptr;
+    if (g_nccl.MemFree) g_nccl.MemFree(p);
+  }
   if (h->comm) g_nccl.CommDestroy(h->comm);
   for (auto& v : h->tev)
     for (cudaEvent_t e : v) cudaEventDestroy(e);
@@ -341,7 +383,8 @@ sma_status timer_pair(sma_handle* h, int phase, cudaEvent_t** out) {
   return SMA_OK;
 }
 
-sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s) {
+sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s, int sms = 0) {
+  if (sms <= 0) sms = h->num_sms;
   ReplicaArgs a{};
   a.W = h->W;
   a.ld = h->d_pad;
@@ -361,10 +404,10 @@ sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s) {
   STATUS_TRY(timer_pair(h, SMA_PHASE_REPLICA, &tp));
   if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
   if (h->r > 0) {
-    CUDA_TRY(launch_replica_step(mode, h->tma, a, h->num_sms, s));
+    CUDA_TRY(launch_replica_step(mode, h->tma, a, sms, s));
     ++h->launches;
     if (h->matc) {
-      CUDA_TRY(launch_reduce_corrections(mode, a, h->num_sms, s));
+      CUDA_TRY(launch_reduce_corrections(mode, a, sms, s));
       ++h->launches;
     }
   } else if (mode == kFused) {
@@ -383,6 +426,31 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
                          cudaStream_t s) {
   const size_t cnt = (size_t)h->shard_len;
   cudaEvent_t* tp = nullptr;
+  if (h->nvls) {  // a6-a8 in one multicast kernel
+    NvlsArgs a{};
+    const size_t part_off = (size_t)(reinterpret_cast<const char*>(partial) -
+                                     reinterpret_cast<const char*>(h->nv.uc));
+    a.part_mc = reinterpret_cast<const float*>(h->nv.mcva + part_off);
+    a.znext_mc = reinterpret_cast<float*>(h->nv.mcva + h->nv_off_z) + (int64_t)(1 - h->cur) * h->d_pad;
+    a.z = h->z();
+    a.zprev = h->zprev();
+    a.off4 = h->shard_off / 4;
+    a.len4 = h->shard_len / 4;
+    a.alpha = h->alpha;
+    a.mu = h->mu;
+    a.coef_b = coef_b;
+    a.flag_uc = reinterpret_cast<unsigned*>(h->nv.uc);
+    a.flag_mc = reinterpret_cast<unsigned*>(h->nv.mcva);
+    a.expect = h->nv_ctl;
+    a.done_ctr = h->nv_ctl + 2;
+    a.n = h->cfg.world;
+    a.nonfinite = h->check ? h->nonfinite : nullptr;
+    STATUS_TRY(timer_pair(h, SMA_PHASE_NVLS_ZSYNC, &tp));
+    if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
+    CUDA_TRY(launch_zsync_nvls(mode, a, h->overlap ? (h->sync_sms > 0 ? h->sync_sms : 1) : h->num_sms, s));
+    if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
+    return SMA_OK;
+  }
   STATUS_TRY(timer_pair(h, SMA_PHASE_REDUCE_SCATTER, &tp));
   if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
   NCCL_TRY(g_nccl.ReduceScatter(partial, h->S, cnt, ncclFloat32, ncclSum, h->comm, s));
@@ -416,7 +484,7 @@ sma_status enqueue_round(sma_handle* h, cudaStream_t s) {
     CUDA_TRY(cudaStreamWaitEvent(h->sB, h->evFork, 0));
     STATUS_TRY(enqueue_zsync(h, kPartialB, Qcur, coef_b, h->sB));
     CUDA_TRY(cudaEventRecord(h->evJoin, h->sB));
-    STATUS_TRY(replica_launch(h, kPartialB, Qnext, s));
+    STATUS_TRY(replica_launch(h, kPartialB, Qnext, s, h->num_sms - h->sync_sms));
     CUDA_TRY(cudaStreamWaitEvent(s, h->evJoin, 0));
     h->launches += 1;  // zsync
   }
@@ -431,6 +499,25 @@ void advance(sma_handle* h) {
 sma_status alloc_zero(float** p, size_t n) {
   CUDA_TRY(cudaMalloc(p, sizeof(float) * n));
   CUDA_TRY(cudaMemset(*p, 0, sizeof(float) * n));
+  return SMA_OK;
+}
+
+// Collective buffer: ncclMemAlloc + ncclCommRegister when available (and
+// SMA_NCCL_MEMALLOC != 0), else cudaMalloc.  Zero-filled.
+sma_status alloc_coll(sma_handle* h, float** p, size_t n) {
+  const char* e = getenv("SMA_NCCL_MEMALLOC");
+  const bool use = g_nccl.MemAlloc && g_nccl.MemFree && !(e && e[0] == '0');
+  if (!use) return alloc_zero(p, n);
+  void* q = nullptr;
+  NCCL_TRY(g_nccl.MemAlloc(&q, sizeof(float) * n));
+  h->nccl_allocs.push_back(q);
+  *p = static_cast<float*>(q);
+  CUDA_TRY(cudaMemset(q, 0, sizeof(float) * n));
+  if (g_nccl.CommRegister) {
+    void* reg = nullptr;
+    if (g_nccl.CommRegister(h->comm, q, sizeof(float) * n, &reg) == ncclSuccess && reg)
+      h->nccl_regs.push_back(reg);
+  }
   return SMA_OK;
 }
 
@@ -450,6 +537,9 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
   h->timing = (f & SMA_FLAG_TIMING) != 0;
   h->graphs = (f & SMA_FLAG_CUDA_GRAPH) != 0 && !h->timing;
   h->check = (f & SMA_FLAG_CHECK_FINITE) != 0;
+  h->nvls = (f & SMA_FLAG_NVLS_ZSYNC) != 0;
+  if (h->nvls && !h->collective)
+    return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_NVLS_ZSYNC needs world > 1 or SMA_FLAG_FORCE_COLLECTIVE");
   h->d_pad = sma_plan_d_pad(cfg->d, cfg->world);
   h->n4 = h->d_pad / 4;
   STATUS_TRY(sma_plan_local_replicas(cfg->k, cfg->world, cfg->rank, &h->j0, &h->r));
@@ -472,32 +562,13 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
                 prop.major, prop.minor);
   h->num_sms = prop.multiProcessorCount;
 
-  const size_t dp = (size_t)h->d_pad;
-  STATUS_TRY(alloc_zero(&h->W, dp * (h->r > 0 ? h->r : 1)));
-  STATUS_TRY(alloc_zero(&h->zbuf, 2 * dp));
-  if (h->collective) {
-    STATUS_TRY(alloc_zero(&h->S, (size_t)h->shard_len));
-    if (h->overlap)
-      STATUS_TRY(alloc_zero(&h->Q, 2 * dp));
-    else
-      STATUS_TRY(alloc_zero(&h->P, dp));
-  }
-  if (h->matc) STATUS_TRY(alloc_zero(&h->C, dp * (h->r > 0 ? h->r : 1)));
-  CUDA_TRY(cudaMalloc(&h->nonfinite, sizeof(int)));
-  CUDA_TRY(cudaMemset(h->nonfinite, 0, sizeof(int)));
   CUDA_TRY(cudaStreamCreateWithFlags(&h->sB, cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&h->sIO, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&h->evFork, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&h->evJoin, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&h->evDone, cudaEventDisableTiming));
-
-  // Alg. 1 line 1-2 (R2) and R3: z = z_prev = w_j = w0; padding stays 0.
-  CUDA_TRY(cudaMemcpy(h->zbuf, w0, sizeof(float) * cfg->d, cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(h->zbuf + dp, h->zbuf, sizeof(float) * dp, cudaMemcpyDeviceToDevice));
-  if (h->r > 0) CUDA_TRY(launch_broadcast_rows(h->W, h->d_pad, h->r, h->zbuf, h->n4, h->num_sms, 0));
-  CUDA_TRY(cudaDeviceSynchronize());
-
-  if (h->collective) {
+  const size_t dp = (size_t)h->d_pad;
+  if (h->collective) {  // the communicator first: the collective buffers come from NCCL
     if (!nccl_load()) return fail(SMA_ERR_NCCL, "cannot load NCCL: %s", g_nccl.why.c_str());
     ncclUniqueId id;
     if (cfg->world > 1) {
@@ -506,7 +577,73 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
       NCCL_TRY(g_nccl.GetUniqueId(&id));
     }
     NCCL_TRY(g_nccl.CommInitRank(&h->comm, cfg->world, id, cfg->rank));
+    if (const char* e = getenv("SMA_SYNC_SMS")) h->sync_sms = atoi(e);
+    if (h->sync_sms < 0) h->sync_sms = 0;
+    if (h->sync_sms > h->num_sms - 1) h->sync_sms = h->num_sms - 1;
   }
+  STATUS_TRY(alloc_zero(&h->W, dp * (h->r > 0 ? h->r : 1)));
+  if (h->nvls) {
+    // [flags (4 KB) | P, or Q[2] | z[2]] bound to one multicast object per rank
+    h->nv_off_part = 4096;
+    h->nv_off_z = h->nv_off_part + sizeof(float) * dp * (h->overlap ? 2 : 1);
+    const size_t bytes = h->nv_off_z + sizeof(float) * 2 * dp;
+    std::string key;
+    {
+      uint64_t x = 1469598103934665603ull;  // FNV-1a of the NCCL id: rendezvous name
+      const unsigned char* b = reinterpret_cast<const unsigned char*>(cfg->nccl_id);
+      if (cfg->world > 1)
+        for (int i = 0; i < SMA_NCCL_ID_BYTES; ++i) x = (x ^ b[i]) * 1099511628211ull;
+      else
+        x ^= (uint64_t)getpid() << 20 ^ (uint64_t)(uintptr_t)h;
+      char buf[32];
+      snprintf(buf, sizeof buf, "%016llx", (unsigned long long)x);
+      key = buf;
+    }
+    int* bar = nullptr;
+    CUDA_TRY(cudaMalloc(&bar, sizeof(int) * cfg->world));
+    auto barrier = [&](std::string* err) -> bool {
+      if (cfg->world == 1) return true;
+      if (g_nccl.AllReduce(bar, bar, 1, ncclInt32, ncclSum, h->comm, h->sIO) != ncclSuccess ||
+          cudaStreamSynchronize(h->sIO) != cudaSuccess) {
+        *err = "NCCL barrier failed";
+        return false;
+      }
+      return true;
+    };
+    std::string err;
+    const bool ok = nvls_setup(&h->nv, h->dev, cfg->rank, cfg->world, bytes, key, barrier, &err);
+    cudaFree(bar);
+    if (!ok) return fail(SMA_ERR_CUDA, "NVLS z-sync setup: %s", err.c_str());
+    h->zbuf = reinterpret_cast<float*>(h->nv.uc + h->nv_off_z);
+    if (h->overlap)
+      h->Q = reinterpret_cast<float*>(h->nv.uc + h->nv_off_part);
+    else
+      h->P = reinterpret_cast<float*>(h->nv.uc + h->nv_off_part);
+    CUDA_TRY(cudaMalloc(&h->nv_ctl, 4 * sizeof(unsigned)));
+    CUDA_TRY(cudaMemset(h->nv_ctl, 0, 4 * sizeof(unsigned)));
+  } else if (h->collective) {
+    // z (the all-gather target), the partial(s) and the reduce-scatter output
+    // are NCCL-allocated and registered, so NCCL can use zero-copy NVLS
+    // (in-switch reduction / multicast) on NVSwitch systems.
+    STATUS_TRY(alloc_coll(h, &h->zbuf, 2 * dp));
+    STATUS_TRY(alloc_coll(h, &h->S, (size_t)h->shard_len));
+    if (h->overlap)
+      STATUS_TRY(alloc_coll(h, &h->Q, 2 * dp));
+    else
+      STATUS_TRY(alloc_coll(h, &h->P, dp));
+  } else {
+    STATUS_TRY(alloc_zero(&h->zbuf, 2 * dp));
+  }
+  if (h->matc) STATUS_TRY(alloc_zero(&h->C, dp * (h->r > 0 ? h->r : 1)));
+  CUDA_TRY(cudaMalloc(&h->nonfinite, sizeof(int)));
+  CUDA_TRY(cudaMemset(h->nonfinite, 0, sizeof(int)));
+
+  // Alg. 1 line 1-2 (R2) and R3: z = z_prev = w_j = w0; padding stays 0.
+  CUDA_TRY(cudaMemcpy(h->zbuf, w0, sizeof(float) * cfg->d, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(h->zbuf + dp, h->zbuf, sizeof(float) * dp, cudaMemcpyDeviceToDevice));
+  if (h->r > 0) CUDA_TRY(launch_broadcast_rows(h->W, h->d_pad, h->r, h->zbuf, h->n4, h->num_sms, 0));
+  CUDA_TRY(cudaDeviceSynchronize());
+
   return SMA_OK;
 }
 }  // namespace

@@ -24,6 +24,7 @@ FLAG_FORCE_COLLECTIVE = 16
 FLAG_TIMING = 32
 FLAG_KERNEL_TMA = 64
 FLAG_KERNEL_LDG = 128
+FLAG_NVLS_ZSYNC = 256
 MAX_LOCAL_REPLICAS = 64
 NCCL_ID_BYTES = 128
 
@@ -254,7 +255,8 @@ def sma_nccl_unique_id() -> bytes:
     return bytes(buf)
 
 
-PHASE_REPLICA, PHASE_REDUCE_SCATTER, PHASE_SHARD_UPDATE, PHASE_ALL_GATHER = 0, 1, 2, 3
+PHASE_REPLICA, PHASE_REDUCE_SCATTER, PHASE_SHARD_UPDATE, PHASE_ALL_GATHER, PHASE_NVLS_ZSYNC = \
+    0, 1, 2, 3, 4
 
 
 def sma_kernel_time(h: int, phase: int = PHASE_REPLICA, reset: bool = False) -> tuple[float, int]:

@@ -19,9 +19,15 @@ else:
              (2, sma.FLAG_FORCE_COLLECTIVE | sma.FLAG_OVERLAP),
              (2, sma.FLAG_FORCE_COLLECTIVE | sma.FLAG_OVERLAP | T),
              (4, L), (4, T), (32, L), (32, T), (16, sma.FLAG_MATERIALIZE_C),
-             (16, sma.FLAG_MATERIALIZE_C | L), (2, sma.FLAG_MATERIALIZE_C)]
+             (16, sma.FLAG_MATERIALIZE_C | L), (2, sma.FLAG_MATERIALIZE_C),
+             (2, sma.FLAG_FORCE_COLLECTIVE | sma.FLAG_NVLS_ZSYNC),
+             (2, sma.FLAG_FORCE_COLLECTIVE | sma.FLAG_NVLS_ZSYNC | sma.FLAG_OVERLAP)]
 for k, flags in cases:
-    h = sma.Sma(d, k, 1.0 / k, 0.1, 0.9, w0, flags=flags | sma.FLAG_TIMING)
+    try:
+        h = sma.Sma(d, k, 1.0 / k, 0.1, 0.9, w0, flags=flags | sma.FLAG_TIMING)
+    except sma.SmaError as e:
+        print(json.dumps({"k": k, "flags": flags, "error": str(e)}), flush=True)
+        continue
     s = torch.cuda.Stream()
     h.synth_grads(0, 2244, s)
     for _ in range(10):
@@ -37,11 +43,13 @@ for k, flags in cases:
     ms = e0.elapsed_time(e1) / steps
     kms, n = h.kernel_time(reset=True)
     kms /= max(n, 1)
+    phases = [h.kernel_time(reset=True, phase=p) for p in range(1, 5)]
     coll = bool(flags & sma.FLAG_FORCE_COLLECTIVE)
     nbytes = 4 * h.d_pad * (3 * k + (2 if coll else 3))
     if flags & sma.FLAG_MATERIALIZE_C:
         nbytes = 4 * h.d_pad * (6 * k + 3)
     print(json.dumps({"k": k, "flags": flags, "tma_cfg": os.environ.get("SMA_TMA_CONFIG", "0"), "ms_per_round": ms, "rounds_s": 1000 / ms,
                       "kernel_ms": kms, "kernel_GBs": nbytes / kms / 1e6,
-                      "frac": nbytes / kms / 1e6 / 6552.6}), flush=True)
+                      "frac": nbytes / kms / 1e6 / 6552.6,
+                      "phase_ms": [pm / pn if pn else 0 for pm, pn in phases]}), flush=True)
     h.close()

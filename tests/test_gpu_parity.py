@@ -49,7 +49,21 @@ COLLECTIVE_FLAGS = {
     "matc_tma": 2 | 64,
     "collA_tma": 16 | 64,
     "collB_tma_graph": 16 | 1 | 8 | 64,
+    "nvlsA": 16 | 256,
+    "nvlsA_matc": 16 | 2 | 256,
+    "nvlsB": 16 | 1 | 256,
+    "nvlsB_graph": 16 | 1 | 8 | 256,
 }
+
+
+def make_sma(S, *args, flags=0, **kw):
+    """Create a handle; NVLS variants skip (loudly) on a device without multicast."""
+    try:
+        return S.Sma(*args, flags=flags, **kw)
+    except S.SmaError as e:
+        if flags & 256 and "multicast" in str(e):
+            pytest.skip(f"NVSwitch multicast unavailable: {e}")
+        raise
 
 
 def dev_read(ptr, n):
@@ -66,7 +80,7 @@ def dev_read(ptr, n):
 
 
 def run_synth_gpu(torch, S, d, k, R, alpha, gamma, mu, flags, stream=None):
-    h = S.Sma(d, k, alpha, gamma, mu, sma_inputs.w0(d), flags=flags)
+    h = make_sma(S, d, k, alpha, gamma, mu, sma_inputs.w0(d), flags=flags)
     stream = stream or torch.cuda.Stream()   # non-default: CUDA-graph variants capture on it
     for i in range(R):
         h.synth_grads(i, sma_inputs.SEED_G, stream)
@@ -88,7 +102,7 @@ def test_dyadic_trace_bitwise(torch_cuda, S, variant, k, alpha, gamma, mu):
     w0 = sma_inputs.dyadic(d, 100 + k)
     G = sma_inputs.dyadic((R, k, d), 200 + k)
     tr = exact.sma_exact(list(w0), G.tolist(), alpha, gamma, mu)
-    h = S.Sma(d, k, alpha, gamma, mu, w0.astype(np.float32), flags=COLLECTIVE_FLAGS[variant])
+    h = make_sma(S, d, k, alpha, gamma, mu, w0.astype(np.float32), flags=COLLECTIVE_FLAGS[variant])
     gd = torch.tensor(G, dtype=torch.float32, device="cuda")
     torch.cuda.synchronize()
     stream = torch.cuda.Stream()
@@ -163,8 +177,8 @@ def test_mode_b_with_distinct_initial_replicas(torch_cuda, S, orc):
     w0 = sma_inputs.w0(d)
     Winit = (w0 + rng.uniform(-0.05, 0.05, (k, d))).astype(np.float32)
     stream = torch_cuda.cuda.Stream()
-    for flags in (0, 16, 16 | 1, 16 | 1 | 8):
-        h = S.Sma(d, k, a, g, m, w0, flags=flags)
+    for flags in (0, 16, 16 | 1, 16 | 1 | 8, 16 | 1 | 256):
+        h = make_sma(S, d, k, a, g, m, w0, flags=flags)
         for j in range(k):
             h.set_replica(j, Winit[j])
         st = orc.State.init(w0, k, Winit.astype(np.float64))
