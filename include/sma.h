@@ -181,6 +181,32 @@ sma_status sma_synth_grads(sma_handle* h, int64_t round, uint64_t seed, void* cu
  * COLLECTIVE when world > 1.  Errors: GRADS_MISSING, CUDA, NCCL. */
 sma_status sma_step(sma_handle* h, void* cuda_stream);
 
+/* Local-only iteration for a synchronisation period tau > 1 (
+ * reading R17 = S:348): every local learner applies only its gradient,
+ * w_j <- w_j - gamma g_j; no correction, z and z_prev unchanged.  Call it on
+ * the tau - 1 non-synchronising iterations and sma_step on every tau-th.  Not
+ * collective.  Errors: GRADS_MISSING, CUDA. */
+sma_status sma_step_local(sma_handle* h, void* cuda_stream);
+
+/* ---------------------------------------------------- auto-tuner (NEXT-4) */
+
+/* Alg. 2, one pass of its loop body over m GPUs (host only):
+ *   if t[g] - t_prev[g] > tau: l[g] += 1;  else if t[g] < t_prev[g] and l[g] > 0:
+ *   l[g] -= 1;  t_prev[g] = t[g].   (Initialise l = 1, t_prev = 0, lines 1-2.)
+ * t: observed learning throughput per GPU (e.g. learner batches/s). */
+sma_status sma_autotune_step(int32_t m, double tau, const double* t, int32_t* l, double* t_prev);
+
+/* Set the number of learners on EVERY GPU to l_new (the same count on all
+ * ranks; k becomes l_new * world).  Rank g keeps its first
+ * min(r, l_new) replicas (global index g*l_new + slot afterwards); each added
+ * replica is initialised with the current z.  alpha is NOT changed
+ * (use sma_set_hparams, e.g. alpha = 1/k).  Gradients registered for kept
+ * learners stay registered; added learners need one.  Synchronises; COLLECTIVE
+ * when world > 1 (every rank calls it with the same l_new).
+ * Errors: INVALID_ARG (l_new outside [0, SMA_MAX_LOCAL_REPLICAS], or 0 on a
+ * single-GPU handle), CUDA, OOM. */
+sma_status sma_set_local_replicas(sma_handle* h, int32_t l_new, void* cuda_stream);
+
 /* ----------------------------------------------------------------- outputs */
 
 /* Copy the central model z (Alg. 1 output) into z_out (d floats;

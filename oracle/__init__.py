@@ -61,6 +61,11 @@ def lib():
         L.orc_sma_run_softmax.argtypes = [i32, i32, i32, P, P, i64, u64, i32, f64, f64, f64,
                                           i64, P, P, P, P]
         L.orc_sma_run_softmax.restype = C.c_int
+        L.orc_local_round.argtypes, L.orc_local_round.restype = [i64, i32, f64, P, P], None
+        L.orc_autotune_step.argtypes = [i32, f64, P, P, P]
+        L.orc_autotune_step.restype = None
+        L.orc_resize_replicas.argtypes = [i64, i32, i32, i32, P, P, P]
+        L.orc_resize_replicas.restype = None
         _lib = L
     return _lib
 
@@ -152,6 +157,22 @@ class State:
         W = np.tile(w0_vec, (k, 1)) if w_init is None else _f64(w_init)
         return cls(W, w0_vec, w0_vec)
 
+    def local_round(self, G, gamma):
+        """Local-only iteration (sync period tau > 1, R17): w_j -= gamma G_j."""
+        k, m = self.W.shape
+        G = _f64(G).reshape(k, m)
+        lib().orc_local_round(m, k, gamma, _p(self.W), _p(G))
+        return self
+
+    def resize(self, n: int, l_new: int):
+        """Uniform per-GPU learner count l -> l_new (NEXT-4); new replicas := z."""
+        k, m = self.W.shape
+        assert k % n == 0
+        Wn = np.empty((n * l_new, m))
+        lib().orc_resize_replicas(m, n, k // n, l_new, _p(self.W), _p(self.z), _p(Wn))
+        self.W = Wn
+        return self
+
     def round(self, G, alpha, gamma, mu):
         """One iteration (Alg. 1 lines 4-14) with raw gradients G [k][m]."""
         k, m = self.W.shape
@@ -199,3 +220,12 @@ def run_softmax(X, y, b, batch_seed, k, alpha, gamma, mu, R, w0_vec, in_dim=784,
     if rc != 0:
         raise ValueError("oracle softmax run failed")
     return z, zp, W
+
+
+def autotune_step(tau: float, t, l, t_prev):
+    """Alg. 2 lines 4-9 over all GPUs; returns new (l, t_prev)."""
+    t = _f64(t)
+    l = np.ascontiguousarray(l, dtype=np.int32).copy()
+    tp = _f64(t_prev).copy()
+    lib().orc_autotune_step(t.size, tau, _p(t), _p(l), _p(tp))
+    return l, tp

@@ -278,3 +278,49 @@ int orc_sma_run_softmax(int32_t in_dim, int32_t classes, int32_t b,
     free(W); free(G); free(cs); free(rows);
     return rc;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-3 / NEXT-4                                           */
+/* ------------------------------------------------------------------------ */
+
+/* Local-only iteration for synchronisation period tau > 1 (PAPER.md:1462-1471,
+ * reading R17 = SPEC S:348): on a non-synchronising iteration every learner
+ * applies only its gradient, w_j <- w_j - gamma G_j (Eq. 1); no correction and
+ * no update of z or z_prev. */
+void orc_local_round(int64_t m, int32_t k, double gamma, double *W, const double *G) {
+    for (int32_t j = 0; j < k; j++)
+        for (int64_t p = 0; p < m; p++)
+            W[(int64_t)j * m + p] = W[(int64_t)j * m + p] - gamma * G[(int64_t)j * m + p];
+}
+
+/* Alg. 2, "Selecting the number of learners per GPU", one
+ * pass of its while-loop body over the m GPUs (lines 4-9):
+ *   if t_g - t'_g > tau:            l_g <- l_g + 1     (line 7)
+ *   else if t_g < t'_g and l_g > 0: l_g <- l_g - 1     (line 8)
+ *   t'_g <- t_g                                         (line 9)
+ * l [m] and t_prev [m] are updated in place; t [m] is the observed
+ * throughput.  Initial values (line 1-2): l = 1, t' = 0. */
+void orc_autotune_step(int32_t m, double tau, const double *t, int32_t *l, double *t_prev) {
+    for (int32_t g = 0; g < m; g++) {
+        if (t[g] - t_prev[g] > tau) l[g] = l[g] + 1;
+        else if (t[g] < t_prev[g] && l[g] > 0) l[g] = l[g] - 1;
+        t_prev[g] = t[g];
+    }
+}
+
+/* Replica resize with the same number l of learners on each of n GPUs
+ * (one GPU's throughput may set the count for all), from l
+ * to l_new: GPU g keeps its first min(l, l_new) replicas in order; each added
+ * replica is initialised with the current central model z ("initialised with
+ * the latest value of the average model").  Global index of
+ * replica s on GPU g is g*l + s before and g*l_new + s after.
+ * W [n*l][m] -> W_new [n*l_new][m]. */
+void orc_resize_replicas(int64_t m, int32_t n, int32_t l, int32_t l_new, const double *W,
+                         const double *z, double *W_new) {
+    for (int32_t g = 0; g < n; g++)
+        for (int32_t s = 0; s < l_new; s++) {
+            double *dst = W_new + ((int64_t)g * l_new + s) * m;
+            const double *src = (s < l) ? W + ((int64_t)g * l + s) * m : z;
+            for (int64_t p = 0; p < m; p++) dst[p] = src[p];
+        }
+}

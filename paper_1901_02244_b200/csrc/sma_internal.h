@@ -23,6 +23,7 @@ enum ReplicaMode : int {
   kFused = 0,    // n == 1: also z_next = z + sum c + mu (z - z_prev)   (Alg. 1 line 13)
   kPartialA = 1, // collective path, paper order: P = sum_{local j} c_j
   kPartialB = 2, // collective path, lookahead: Q = sum_{local j} (w_j' - z)
+  kLocal = 3,    // local-only iteration (sync period tau > 1): w_j' = w_j - gamma g_j
 };
 
 struct ReplicaArgs {

@@ -66,6 +66,13 @@ __device__ __forceinline__ float central_elem(float z, float csum, float zp, flo
 template <int MODE>
 __device__ __forceinline__ void replica_update4(float4& w, const float4 g, const float4 z,
                                                float4& acc, float4& c4, float alpha, float gamma) {
+  if (MODE == kLocal) {  // no correction, no central model (R17): w' = w - gamma g
+    w.x = __fmaf_rn(-gamma, g.x, w.x);
+    w.y = __fmaf_rn(-gamma, g.y, w.y);
+    w.z = __fmaf_rn(-gamma, g.z, w.z);
+    w.w = __fmaf_rn(-gamma, g.w, w.w);
+    return;
+  }
   StepOut o;
   o = sma_elem(w.x, g.x, z.x, alpha, gamma); w.x = o.wn; c4.x = o.c;
   o = sma_elem(w.y, g.y, z.y, alpha, gamma); w.y = o.wn; c4.y = o.c;
@@ -99,6 +106,7 @@ constexpr int kUJ = 4;
 template <int MODE>
 __device__ __forceinline__ void replica_finish(const ReplicaArgs& a, int64_t p0, const float4 z,
                                                const float4 acc, bool& bad) {
+  if (MODE == kLocal) return;
   if (MODE == kFused) {
     const float4 zp = ld_rw(a.zprev_next + p0);
     float4 zn;
@@ -121,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 4) replica_step_ldg(const ReplicaArg
   bool bad = false;
   for (int64_t c = a.c0 + (int64_t)blockIdx.x * kThreads + threadIdx.x; c < dfull4; c += stride) {
     const int64_t p0 = c << 2;
-    const float4 z = ld_ro(a.z + p0);
+    const float4 z = MODE == kLocal ? make_float4(0.f, 0.f, 0.f, 0.f) : ld_ro(a.z + p0);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 c4;
     int j = 0;
@@ -154,7 +162,7 @@ __global__ void __launch_bounds__(kThreads, 4) replica_step_ldg(const ReplicaArg
   const int64_t tail0 = dfull4 > a.c0 ? dfull4 : a.c0;
   for (int64_t c = tail0 + (int64_t)blockIdx.x * kThreads + threadIdx.x; c < a.n4; c += stride) {
     const int64_t p0 = c << 2;
-    const float4 z = ld_ro(a.z + p0);
+    const float4 z = MODE == kLocal ? make_float4(0.f, 0.f, 0.f, 0.f) : ld_ro(a.z + p0);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 c4;
     for (int j = 0; j < a.r; ++j) {
@@ -419,7 +427,7 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
                                 cudaStream_t s) {
   ReplicaArgs a = a0;
   a.c0 = 0;
-  if (tma) {  // TMA-staged full tiles, then the LDG kernel for the rest
+  if (tma && mode != kLocal) {  // TMA-staged full tiles, then the LDG kernel for the rest
     const int64_t nt = tma_full_tiles(a.d);
     cudaError_t e = launch_replica_step_tma(mode, a, nt, num_sms, s);
     if (e != cudaSuccess) return e;
@@ -440,6 +448,11 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
     }
     case kPartialB: {
       auto k = replica_step_ldg<kPartialB>;
+      k<<<grid_for(k, kThreads, 0, work, num_sms), kThreads, 0, s>>>(a);
+      break;
+    }
+    case kLocal: {
+      auto k = replica_step_ldg<kLocal>;
       k<<<grid_for(k, kThreads, 0, work, num_sms), kThreads, 0, s>>>(a);
       break;
     }

@@ -411,7 +411,8 @@ sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s, i
       ++h->launches;
     }
   } else if (mode == kFused) {
-    return fail(SMA_ERR_STATE, "no local replicas on a single-rank handle");
+    CUDA_TRY(launch_replica_step(mode, false, a, sms, s));  // z <- z + mu (z - z_prev)
+    ++h->launches;
   } else {
     CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * h->d_pad, s));
   }
@@ -774,6 +775,98 @@ sma_status sma_step(sma_handle* h, void* stream) {
   }
   advance(h);
   return mark_done(h, s);
+}
+
+sma_status sma_step_local(sma_handle* h, void* stream) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  for (int i = 0; i < h->r; ++i)
+    if (!h->gptr[i])
+      return fail(SMA_ERR_GRADS_MISSING, "learner %d has no registered gradient", h->j0 + i);
+  if (h->r == 0) return SMA_OK;
+  DeviceGuard guard(h->dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  ReplicaArgs a{};
+  a.W = h->W;
+  a.ld = h->d_pad;
+  a.r = h->r;
+  for (int i = 0; i < h->r; ++i) a.g.p[i] = h->gptr[i];
+  a.d = h->cfg.d;
+  a.n4 = h->n4;
+  a.gamma = h->gamma;
+  a.nonfinite = h->check ? h->nonfinite : nullptr;
+  CUDA_TRY(launch_replica_step(kLocal, false, a, h->num_sms, s));
+  ++h->launches;
+  h->q_dirty = true;  // Mode B: Q^i = sum_j (w_j - z_prev) must be recomputed
+  return mark_done(h, s);
+}
+
+sma_status sma_set_local_replicas(sma_handle* h, int32_t l_new, void* stream) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (l_new < 0 || l_new > SMA_MAX_LOCAL_REPLICAS)
+    return fail(SMA_ERR_INVALID_ARG, "l_new=%d outside [0, %d]", l_new, SMA_MAX_LOCAL_REPLICAS);
+  if (!h->collective && l_new == 0)
+    return fail(SMA_ERR_INVALID_ARG, "a single-GPU handle needs at least one replica");
+  DeviceGuard guard(h->dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  STATUS_TRY(sync_handle(h));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  const size_t dp = (size_t)h->d_pad;
+  const int keep = h->r < l_new ? h->r : l_new;
+  float* W2 = nullptr;
+  STATUS_TRY(alloc_zero(&W2, dp * (l_new > 0 ? l_new : 1)));
+  if (keep > 0)
+    CUDA_TRY(cudaMemcpyAsync(W2, h->W, sizeof(float) * dp * keep, cudaMemcpyDeviceToDevice, s));
+  if (l_new > keep)  // added learners start from the current central model
+    CUDA_TRY(launch_broadcast_rows(W2 + dp * keep, h->d_pad, l_new - keep, h->z(), h->n4,
+                                   h->num_sms, s));
+  float* G2 = nullptr;
+  float* C2 = nullptr;
+  if (h->G) {
+    STATUS_TRY(alloc_zero(&G2, dp * (l_new > 0 ? l_new : 1)));
+    if (keep > 0)
+      CUDA_TRY(cudaMemcpyAsync(G2, h->G, sizeof(float) * dp * keep, cudaMemcpyDeviceToDevice, s));
+  }
+  if (h->matc) STATUS_TRY(alloc_zero(&C2, dp * (l_new > 0 ? l_new : 1)));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  // re-point registrations: internal buffers move, borrowed pointers stay
+  const float* gp[SMA_MAX_LOCAL_REPLICAS] = {};
+  for (int i = 0; i < keep; ++i) {
+    const float* old = h->gptr[i];
+    if (h->G && old >= h->G && old < h->G + dp * h->r)
+      gp[i] = G2 + (old - h->G);
+    else
+      gp[i] = old;
+  }
+  cudaFree(h->W);
+  h->W = W2;
+  if (h->G) {
+    cudaFree(h->G);
+    h->G = G2;
+  }
+  if (h->matc) {
+    cudaFree(h->C);
+    h->C = C2;
+  }
+  for (int i = 0; i < SMA_MAX_LOCAL_REPLICAS; ++i) h->gptr[i] = gp[i];
+  h->r = l_new;
+  h->cfg.k = l_new * h->cfg.world;
+  h->j0 = h->cfg.rank * l_new;
+  h->q_dirty = true;
+  ++h->ver;
+  return mark_done(h, s);
+}
+
+sma_status sma_autotune_step(int32_t m, double tau, const double* t, int32_t* l, double* t_prev) {
+  if (m < 1 || !t || !l || !t_prev) return fail(SMA_ERR_INVALID_ARG, "bad auto-tuner arguments");
+  for (int32_t g = 0; g < m; ++g) {
+    const double dt = t[g] - t_prev[g];
+    if (dt > tau)
+      ++l[g];                          // Alg. 2 line 7: significant increase -> add a learner
+    else if (t[g] < t_prev[g] && l[g] > 0)
+      --l[g];                          // line 8: decrease -> remove one
+    t_prev[g] = t[g];                  // line 9
+  }
+  return SMA_OK;
 }
 
 static sma_status copy_out(sma_handle* h, const float* src, float* out, int out_is_device) {

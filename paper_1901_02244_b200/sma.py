@@ -40,7 +40,8 @@ EXPORTS = ["sma_create", "sma_destroy", "sma_set_learner_grads", "sma_set_learne
            "sma_learner_attach", "sma_learner_grads", "sma_plan_d_pad",
            "sma_plan_replica_location", "sma_plan_local_replicas", "sma_plan_shard_range",
            "sma_plan_batch_indices", "sma_nccl_unique_id", "sma_kernel_time",
-           "sma_launch_count", "sma_info", "sma_last_error", "sma_abi_version"]
+           "sma_launch_count", "sma_info", "sma_last_error", "sma_abi_version",
+           "sma_step_local", "sma_autotune_step", "sma_set_local_replicas"]
 
 
 class SmaError(RuntimeError):
@@ -99,6 +100,9 @@ def load():
                       C.POINTER(i64)], st),
         "sma_last_error": ([], C.c_char_p),
         "sma_abi_version": ([], C.c_int),
+        "sma_step_local": ([P, P], st),
+        "sma_autotune_step": ([i32, C.c_double, P, P, P], st),
+        "sma_set_local_replicas": ([P, i32, P], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -158,6 +162,24 @@ def sma_synth_grads(h: int, rnd: int, seed: int, stream=None) -> None:
 
 def sma_step(h: int, stream=None) -> None:
     _check(load().sma_step(h, _stream(stream)), "sma_step")
+
+
+def sma_step_local(h: int, stream=None) -> None:
+    _check(load().sma_step_local(h, _stream(stream)), "sma_step_local")
+
+
+def sma_autotune_step(tau: float, t, l, t_prev):
+    """Alg. 2 loop body over all GPUs; returns the new (l, t_prev) arrays."""
+    t = np.ascontiguousarray(t, np.float64)
+    l = np.ascontiguousarray(l, np.int32).copy()
+    tp = np.ascontiguousarray(t_prev, np.float64).copy()
+    _check(load().sma_autotune_step(t.size, tau, t.ctypes.data, l.ctypes.data, tp.ctypes.data),
+           "sma_autotune_step")
+    return l, tp
+
+
+def sma_set_local_replicas(h: int, l_new: int, stream=None) -> None:
+    _check(load().sma_set_local_replicas(h, l_new, _stream(stream)), "sma_set_local_replicas")
 
 
 def sma_get_central(h: int, out, out_is_device: bool) -> None:
@@ -335,6 +357,15 @@ class Sma:
 
     def step(self, stream=None):
         sma_step(self.h, stream)
+
+    def step_local(self, stream=None):
+        sma_step_local(self.h, stream)
+
+    def set_local_replicas(self, l_new, stream=None):
+        sma_set_local_replicas(self.h, l_new, stream)
+        info = sma_info(self.h)
+        self.local_first, self.local_count = info["local_first"], info["local_count"]
+        self.k = self.local_count * self.world
 
     def central(self) -> np.ndarray:
         out = np.empty(self.d, np.float32)

@@ -99,3 +99,18 @@ def test_binding_refuses_missing_library(monkeypatch, tmp_path):
     monkeypatch.setattr(sma, "LIB_PATH", str(tmp_path / "libsma.so"))
     with pytest.raises(ImportError):
         sma.load()
+
+
+def test_autotune_matches_oracle(lib, orc):
+    """libsma's Alg. 2 (independent implementation) == the oracle's, on random
+    throughput traces, including the l > 0 guard."""
+    rng = np.random.default_rng(4)
+    for trial in range(50):
+        m = int(rng.integers(1, 9))
+        l = rng.integers(0, 4, m)
+        tp = rng.uniform(0, 100, m)
+        t = tp + rng.uniform(-20, 20, m)
+        tau = float(rng.uniform(0, 10))
+        a = sma.sma_autotune_step(tau, t, l, tp)
+        b = orc.autotune_step(tau, t, l, tp)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])

@@ -360,3 +360,80 @@ def test_host_gradient_path_and_timing(torch_cuda, S, orc):
     ms, n = h.kernel_time()
     assert n == R and ms > 0
     h.close()
+
+
+# ------------------------------------------------- NEXT-3 / NEXT-4 on the GPU
+@pytest.mark.parametrize("flags", [0, 16, 16 | 1, 16 | 1 | 8])
+def test_sync_period_tau(torch_cuda, S, orc, flags):
+    """Synchronise every tau = 3 iterations (R17): sma_step_local
+    on the others; 30 iterations vs the oracle."""
+    d, k, tau = 20_011, 4, 3
+    a, g, m = F32(0.25), F32(0.1), F32(0.9)
+    s = torch_cuda.cuda.Stream()
+    h = S.Sma(d, k, a, g, m, sma_inputs.w0(d), flags=flags)
+    st = orc.State.init(sma_inputs.w0(d), k)
+    for i in range(30):
+        h.synth_grads(i, sma_inputs.SEED_G, s)
+        G = np.stack([sma_inputs.grad(i, j, k, d) for j in range(k)])
+        if (i + 1) % tau == 0:
+            h.step(s)
+            st.round(G, a, g, m)
+        else:
+            h.step_local(s)
+            st.local_round(G, g)
+    assert relerr(h.central(), st.z) <= TOL
+    assert relerr(h.central_prev(), st.z_prev) <= TOL
+    for j in range(k):
+        assert relerr(h.replica(j), st.W[j]) <= TOL
+    h.close()
+
+
+def test_easgd_differs_by_momentum_term(torch_cuda, S):
+    """EA-SGD is Alg. 1 without mu (z - z_prev); from the same
+    state, one round of SMA and of EA-SGD (mu = 0) differ on z by exactly
+    mu (z - z_prev) (to fp32 rounding)."""
+    d, k = 10_001, 4
+    s = torch_cuda.cuda.Stream()
+    hs = [S.Sma(d, k, 0.25, F32(0.1), F32(0.9), sma_inputs.w0(d)) for _ in range(2)]
+    for h in hs:
+        for i in range(5):
+            h.synth_grads(i, sma_inputs.SEED_G, s)
+            h.step(s)
+    z, zp = hs[0].central().astype(np.float64), hs[0].central_prev().astype(np.float64)
+    hs[1].set_hparams(0.25, F32(0.1), 0.0)
+    for h in hs:
+        h.synth_grads(5, sma_inputs.SEED_G, s)
+        h.step(s)
+    diff = hs[0].central().astype(np.float64) - hs[1].central().astype(np.float64)
+    np.testing.assert_allclose(diff, F32(0.9) * (z - zp), rtol=0, atol=2e-7)
+    for h in hs:
+        h.close()
+
+
+@pytest.mark.parametrize("flags", [0, 16, 16 | 1])
+def test_resize_learners(torch_cuda, S, orc, flags):
+    """NEXT-4 resize: k = 4 -> 6 -> 3 learners mid-run with alpha
+    re-set to 1/k; added replicas start from z; vs the oracle."""
+    d = 30_007
+    g_, m_ = F32(0.1), F32(0.9)
+    s = torch_cuda.cuda.Stream()
+    k = 4
+    h = S.Sma(d, k, F32(1 / k), g_, m_, sma_inputs.w0(d), flags=flags)
+    st = orc.State.init(sma_inputs.w0(d), k)
+    rnd = 0
+    for k_new in (4, 6, 3):
+        if k_new != k:
+            h.set_local_replicas(k_new, s)
+            h.set_hparams(F32(1 / k_new), g_, m_)
+            st.resize(1, k_new)
+            k = k_new
+        for _ in range(10):
+            h.synth_grads(rnd, sma_inputs.SEED_G, s)
+            h.step(s)
+            st.round(np.stack([sma_inputs.grad(rnd, j, k, d) for j in range(k)]), F32(1 / k), g_, m_)
+            rnd += 1
+    assert h.local_count == 3
+    assert relerr(h.central(), st.z) <= TOL
+    for j in range(3):
+        assert relerr(h.replica(j), st.W[j]) <= TOL
+    h.close()

@@ -384,3 +384,61 @@ def test_batches_within_an_epoch_are_disjoint(orc):
     assert len(set(seen)) == len(seen) == E * k * b and min(seen) >= 0 and max(seen) < N
     nxt = orc.batch_indices(N, k, b, 42, E, 0)
     assert np.array_equal(nxt, orc.epoch_permutation(N, 42, 1)[:b])
+
+
+# ------------------------------------------------ NEXT-3 / NEXT-4 functions
+def test_local_round_is_sgd_and_leaves_z(orc):
+    """tau > 1 local iterations (R17): tau local rounds equal tau rounds
+    of alpha = 0 SMA on the replicas (itself pinned to Eq. 1 above), and leave z,
+    z_prev untouched; with tau = 1 the schedule is plain SMA."""
+    k, m, tau = 3, 13, 4
+    st, rng = _rand_state(orc, k, m, 30)
+    ref = orc.State(st.W, st.z, st.z_prev)
+    z0, zp0 = st.z.copy(), st.z_prev.copy()
+    for i in range(tau):
+        G = rng.uniform(-1, 1, (k, m))
+        st.local_round(G, F32(0.1))
+        ref.round(G, 0.0, F32(0.1), 0.0)
+    np.testing.assert_allclose(st.W, ref.W, rtol=0, atol=1e-15)
+    assert np.array_equal(st.z, z0) and np.array_equal(st.z_prev, zp0)
+
+
+def test_alg2_worked_examples(orc):
+    """Alg. 2 lines 7-9 on SPEC's examples (tests/golden/alg2_examples.json)."""
+    g = json.load(open(os.path.join(GOLDEN, "alg2_examples.json")))
+    for ex in g["examples"]:
+        l, tp = orc.autotune_step(ex["tau"], [ex["t"]], [ex["l"]], [ex["t_prev"]])
+        assert l[0] == ex["l_after"] and tp[0] == ex["t"]
+
+
+def test_alg2_settles_at_throughput_peak(orc):
+    """S:500 / S:745 (AC6): against a concave throughput curve peaking at l* = 3
+    the tuner reaches l in {3, 4} within 6 rounds, oscillates by at most one
+    afterwards and never reaches 0 (add on increase > tau, remove on
+    decrease).  Two GPUs with different curves adapt independently."""
+    f = [lambda l: 100.0 - 10.0 * (l - 3) ** 2, lambda l: 80.0 - 2.0 * (l - 5) ** 2]
+    l, tp = np.array([1, 1]), np.array([0.0, 0.0])   # Alg. 2 lines 1-2
+    hist = []
+    for it in range(20):
+        t = [f[g](l[g]) for g in range(2)]
+        l, tp = orc.autotune_step(4.0, t, l, tp)
+        hist.append(l.copy())
+    assert all(h[0] >= 1 and h[1] >= 1 for h in hist)
+    assert all(h[0] in (3, 4) for h in hist[5:])
+    assert all(h[1] in (5, 6) for h in hist[10:])
+
+
+def test_resize_keeps_replicas_and_seeds_from_z(orc):
+    """an added replica starts from the current central model; the
+    kept replicas of every GPU are unchanged (uniform count per GPU)."""
+    n, l, m = 2, 3, 5
+    st, _ = _rand_state(orc, n * l, m, 31)
+    W0 = st.W.copy()
+    st.resize(n, 5)
+    assert st.W.shape == (n * 5, m)
+    for g in range(n):
+        assert np.array_equal(st.W[g * 5:g * 5 + 3], W0[g * 3:g * 3 + 3])
+        assert np.array_equal(st.W[g * 5 + 3], st.z) and np.array_equal(st.W[g * 5 + 4], st.z)
+    st.resize(n, 2)
+    for g in range(n):
+        assert np.array_equal(st.W[g * 2:g * 2 + 2], W0[g * 3:g * 3 + 2])
