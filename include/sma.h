@@ -247,9 +247,12 @@ sma_status sma_check_finite(sma_handle* h, int* flag);
 
 /* --------------------------------------------------- built-in learner (a2') */
 
-/* Attach the built-in learner (kind 0 = softmax regression):
- * params layout W [classes][in_dim] row-major then b [classes] (R12), so
- * d must equal classes*in_dim + classes.  X_dev: n_samples x in_dim fp32
+/* Attach the built-in learner: kind 0 = softmax regression,
+ * params W [classes][in_dim] row-major then b [classes] (R12), d =
+ * classes*in_dim + classes; kind 1 = MLP in_dim-hidden-classes with ReLU
+ * (NEXT-2), params W1 [hidden][in_dim], b1 [hidden], W2 [classes]
+ * [hidden], b2 [classes], d = hidden*in_dim + hidden + classes*hidden + classes
+ * (the ReLU mask is decided on fp64 pre-activations, R18).  X_dev: n_samples x in_dim fp32
  * row-major, y_dev: n_samples int32 labels in [0, classes); both on this
  * rank's device and BORROWED for the handle's lifetime.  batch = b rows per
  * learner per round; batch_seed keys the per-epoch permutation (R10).
@@ -260,7 +263,8 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
 
 /* For every local learner j: gather batch B(round, j) (R10), compute the
  * batch-mean gradient (Eq. 2) of the mean cross-entropy at the
- * current replica w_j (max-subtracted softmax, R16) in fp32 FFMA (no TF32),
+ * current replica w_j (max-subtracted softmax, R16) in fp32 FFMA (no TF32;
+ * MLP first-layer pre-activations in fp64),
  * into the handle's gradient buffer, and register it.  Enqueued on
  * cuda_stream.  Errors: STATE (no learner attached), CUDA. */
 sma_status sma_learner_grads(sma_handle* h, int64_t round, void* cuda_stream);

@@ -66,6 +66,8 @@ def lib():
         L.orc_autotune_step.restype = None
         L.orc_resize_replicas.argtypes = [i64, i32, i32, i32, P, P, P]
         L.orc_resize_replicas.restype = None
+        L.orc_mlp_loss_grad.argtypes = [i32, i32, i32, i32, P, P, P, P, P, P]
+        L.orc_mlp_loss_grad.restype = f64
         _lib = L
     return _lib
 
@@ -229,3 +231,20 @@ def autotune_step(tau: float, t, l, t_prev):
     tp = _f64(t_prev).copy()
     lib().orc_autotune_step(t.size, tau, _p(t), _p(l), _p(tp))
     return l, tp
+
+
+def mlp_loss_grad(X, y, rows, params, in_dim=784, hidden=256, classes=10, want_grad=True):
+    """MLP learner (kind 1): (loss, grad or None, min |pre-activation|)."""
+    X = np.ascontiguousarray(X, np.float32)
+    y = np.ascontiguousarray(y, np.int32)
+    rows = _i64(rows)
+    params = _f64(params)
+    g = np.empty_like(params) if want_grad else None
+    mn = C.c_double()
+    loss = lib().orc_mlp_loss_grad(in_dim, hidden, classes, rows.size, _p(X), _p(y), _p(rows),
+                                   _p(params), _p(g) if want_grad else None, C.byref(mn))
+    return float(loss), g, mn.value
+
+
+def mlp_dims(in_dim=784, hidden=256, classes=10) -> int:
+    return hidden * in_dim + hidden + classes * hidden + classes

@@ -324,3 +324,69 @@ void orc_resize_replicas(int64_t m, int32_t n, int32_t l, int32_t l_new, const d
             for (int64_t p = 0; p < m; p++) dst[p] = src[p];
         }
 }
+
+/* ------------------------------------------------------------------------ */
+/* Built-in learner, kind 1: MLP in_dim-hidden-classes with ReLU (SPEC.md    */
+/* S:104 "MLP (784-256-10)"; back-propagation; batch-mean   */
+/* gradient Eq. 2).  Parameter layout (R12): W1 [hidden]    */
+/* [in_dim], b1 [hidden], W2 [classes][hidden], b2 [classes].  ReLU'(a) = 1  */
+/* if a > 0 else 0 (R18).  All fp64.  Returns the mean cross-entropy; fills  */
+/* grad (if not NULL) and, if min_abs_pre != NULL, the smallest |a1| seen   */
+/* (distance of the batch from a ReLU kink).                                  */
+/* ------------------------------------------------------------------------ */
+double orc_mlp_loss_grad(int32_t in_dim, int32_t hidden, int32_t classes, int32_t b,
+                         const float *X, const int32_t *y, const int64_t *rows,
+                         const double *params, double *grad, double *min_abs_pre) {
+    const double *W1 = params;
+    const double *b1 = W1 + (int64_t)hidden * in_dim;
+    const double *W2 = b1 + hidden;
+    const double *b2 = W2 + (int64_t)classes * hidden;
+    int64_t dparams = (int64_t)hidden * in_dim + hidden + (int64_t)classes * hidden + classes;
+    double *a1 = (double *)malloc(sizeof(double) * (size_t)hidden);
+    double *h = (double *)malloc(sizeof(double) * (size_t)hidden);
+    double *logit = (double *)malloc(sizeof(double) * (size_t)classes);
+    double *e = (double *)malloc(sizeof(double) * (size_t)classes);
+    double loss = 0.0, mn = INFINITY;
+    if (grad) for (int64_t q = 0; q < dparams; q++) grad[q] = 0.0;
+    double *gW1 = grad, *gb1 = grad ? grad + (int64_t)hidden * in_dim : NULL;
+    double *gW2 = grad ? gb1 + hidden : NULL, *gb2 = grad ? gW2 + (int64_t)classes * hidden : NULL;
+    for (int32_t t = 0; t < b; t++) {
+        const float *x = X + rows[t] * (int64_t)in_dim;
+        const int32_t yt = y[rows[t]];
+        for (int32_t k = 0; k < hidden; k++) {              /* forward, layer 1 */
+            double s = b1[k];
+            for (int32_t f = 0; f < in_dim; f++) s += W1[(int64_t)k * in_dim + f] * (double)x[f];
+            a1[k] = s;
+            h[k] = s > 0.0 ? s : 0.0;
+            if (fabs(s) < mn) mn = fabs(s);
+        }
+        for (int32_t c = 0; c < classes; c++) {             /* forward, layer 2 */
+            double s = b2[c];
+            for (int32_t k = 0; k < hidden; k++) s += W2[(int64_t)c * hidden + k] * h[k];
+            logit[c] = s;
+        }
+        double mx = logit[0];
+        for (int32_t c = 1; c < classes; c++) if (logit[c] > mx) mx = logit[c];
+        double den = 0.0;
+        for (int32_t c = 0; c < classes; c++) den += exp(logit[c] - mx);
+        loss += -((logit[yt] - mx) - log(den));
+        if (!grad) continue;
+        for (int32_t c = 0; c < classes; c++)               /* dL/dlogits */
+            e[c] = exp(logit[c] - mx) / den - (c == yt ? 1.0 : 0.0);
+        for (int32_t c = 0; c < classes; c++) {
+            for (int32_t k = 0; k < hidden; k++) gW2[(int64_t)c * hidden + k] += e[c] * h[k];
+            gb2[c] += e[c];
+        }
+        for (int32_t k = 0; k < hidden; k++) {              /* back through ReLU */
+            double dh = 0.0;
+            for (int32_t c = 0; c < classes; c++) dh += W2[(int64_t)c * hidden + k] * e[c];
+            double da = a1[k] > 0.0 ? dh : 0.0;
+            for (int32_t f = 0; f < in_dim; f++) gW1[(int64_t)k * in_dim + f] += da * (double)x[f];
+            gb1[k] += da;
+        }
+    }
+    if (grad) for (int64_t q = 0; q < dparams; q++) grad[q] = grad[q] / (double)b;
+    if (min_abs_pre) *min_abs_pre = mn;
+    free(a1); free(h); free(logit); free(e);
+    return loss / (double)b;
+}

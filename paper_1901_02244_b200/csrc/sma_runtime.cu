@@ -252,7 +252,9 @@ struct sma_handle {
 
   // learner
   bool learner = false;
-  int in_dim = 0, classes = 0, batch = 0;
+  int kind = 0, in_dim = 0, hidden = 0, classes = 0, batch = 0;
+  double* mlp_A1 = nullptr;  // MLP scratch, sized for SMA_MAX_LOCAL_REPLICAS learners
+  float* mlp_DA = nullptr;
   const float* X = nullptr;
   const int32_t* y = nullptr;
   int64_t n_samples = 0;
@@ -329,6 +331,8 @@ void free_all(sma_handle* h) {
   cudaFree(h->G);
   cudaFree(h->nonfinite);
   for (int i = 0; i < 2; ++i) cudaFree(h->perm_dev[i]);
+  cudaFree(h->mlp_A1);
+  cudaFree(h->mlp_DA);
   if (h->perm_host) cudaFreeHost(h->perm_host);
   delete h;
 }
@@ -979,17 +983,21 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
                               int32_t classes, int32_t batch, const float* X_dev,
                               const int32_t* y_dev, int64_t n_samples, uint64_t batch_seed) {
   if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
-  (void)hidden;
-  if (kind != 0) return fail(SMA_ERR_INVALID_ARG, "learner kind %d not available (0 = softmax)", kind);
-  if (in_dim < 1 || classes < 2 || batch < 1 || batch > 64 || !X_dev || !y_dev)
+  if (kind != 0 && kind != 1)
+    return fail(SMA_ERR_INVALID_ARG, "learner kind %d not available (0 softmax, 1 mlp)", kind);
+  if (in_dim < 1 || classes < 2 || batch < 1 || batch > 64 || !X_dev || !y_dev ||
+      (kind == 1 && (hidden < 1 || hidden > 4096)))
     return fail(SMA_ERR_INVALID_ARG, "bad learner arguments");
-  if ((int64_t)classes * in_dim + classes != h->cfg.d)
-    return fail(SMA_ERR_INVALID_ARG, "d=%lld != classes*in_dim+classes=%lld", (long long)h->cfg.d,
-                (long long)classes * in_dim + classes);
+  const int64_t dl = kind == 0 ? (int64_t)classes * in_dim + classes
+                               : (int64_t)hidden * in_dim + hidden + (int64_t)classes * hidden + classes;
+  if (dl != h->cfg.d)
+    return fail(SMA_ERR_INVALID_ARG, "d=%lld does not match the learner's %lld parameters",
+                (long long)h->cfg.d, (long long)dl);
   if (n_samples < (int64_t)h->cfg.k * batch || n_samples > INT32_MAX)
     return fail(SMA_ERR_INVALID_ARG, "n_samples must be in [k*batch, 2^31)");
-  if ((size_t)batch * in_dim * sizeof(float) > 200 * 1024)
-    return fail(SMA_ERR_INVALID_ARG, "batch*in_dim too large for shared memory");
+  if ((size_t)batch * in_dim * sizeof(float) > 200 * 1024 ||
+      (kind == 1 && (size_t)batch * (hidden + classes) * sizeof(float) > 200 * 1024))
+    return fail(SMA_ERR_INVALID_ARG, "batch too large for shared memory");
   DeviceGuard guard(h->dev);
   STATUS_TRY(sync_handle(h));
   for (int i = 0; i < 2; ++i) {
@@ -1002,7 +1010,18 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
   h->perm_host = nullptr;
   CUDA_TRY(cudaMallocHost(&h->perm_host, sizeof(int32_t) * (size_t)n_samples));
   STATUS_TRY(ensure_G(h));
+  if (kind == 1) {
+    cudaFree(h->mlp_A1);
+    cudaFree(h->mlp_DA);
+    h->mlp_A1 = nullptr;
+    h->mlp_DA = nullptr;
+    const size_t n = (size_t)SMA_MAX_LOCAL_REPLICAS * batch * hidden;
+    CUDA_TRY(cudaMalloc(&h->mlp_A1, sizeof(double) * n));
+    CUDA_TRY(cudaMalloc(&h->mlp_DA, sizeof(float) * n));
+  }
   h->learner = true;
+  h->kind = kind;
+  h->hidden = hidden;
   h->in_dim = in_dim;
   h->classes = classes;
   h->batch = batch;
@@ -1034,9 +1053,15 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
     h->perm_epoch[buf] = e;
   }
   const int64_t pos0 = (round % E) * h->cfg.k * (int64_t)h->batch;
-  CUDA_TRY(launch_softmax_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim, h->classes,
-                               h->W, h->d_pad, h->r, h->j0, h->G, s));
-  ++h->launches;
+  if (h->kind == 0) {
+    CUDA_TRY(launch_softmax_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim,
+                                 h->classes, h->W, h->d_pad, h->r, h->j0, h->G, s));
+    ++h->launches;
+  } else {
+    CUDA_TRY(launch_mlp_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim, h->hidden,
+                             h->classes, h->W, h->d_pad, h->r, h->j0, h->mlp_A1, h->mlp_DA, h->G, s));
+    h->launches += 3;
+  }
   for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
   return mark_done(h, s);
 }

@@ -437,3 +437,63 @@ def test_resize_learners(torch_cuda, S, orc, flags):
     for j in range(3):
         assert relerr(h.replica(j), st.W[j]) <= TOL
     h.close()
+
+
+# ------------------------------------------------------- NEXT-2: MLP learner
+MLP_D = 256 * 784 + 256 + 10 * 256 + 10
+
+
+def test_mlp_gradient_single_round(torch_cuda, S, orc):
+    """One MLP learner gradient (gamma = 1, alpha = mu = 0 gives w' = w - g) at a
+    random point vs the fp64 oracle gradient of the same batch (R10); the ReLU
+    mask is decided in fp64 on both sides (R18) and the batch is checked to be
+    away from kinks."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(2_000, seed=12)
+    k, b = 3, 16
+    w0 = np.random.default_rng(5).normal(0, 0.05, MLP_D).astype(np.float32)
+    h = S.Sma(MLP_D, k, 0.0, 1.0, 0.0, w0)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    S.sma_learner_attach(h.h, 1, 784, 256, 10, b, Xd, yd, X.shape[0], 21)
+    rnd = 50   # crosses an epoch boundary (E = 41)
+    S.sma_learner_grads(h.h, rnd, torch.cuda.current_stream())
+    h.step()
+    for j in range(k):
+        rows = orc.batch_indices(X.shape[0], k, b, 21, rnd, j)
+        _, gref, margin = orc.mlp_loss_grad(X, y, rows, w0.astype(np.float64))
+        assert margin > 1e-9
+        gpu = w0.astype(np.float64) - h.replica(j)
+        assert np.max(np.abs(gpu - gref)) < 2e-6
+    h.close()
+
+
+def test_mlp_learner_sma_parity(torch_cuda, S, orc):
+    """SMA with the MLP learner in the loop (k = 2, b = 8, 30 rounds) vs the fp64
+    oracle.  Parity is conditioned on no pre-activation coming within the
+    fp32-vs-fp64 state divergence of a ReLU kink (the mask is an integer
+    decision, R18); the oracle's margin is asserted every round."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(4_000, seed=13)
+    k, b, R = 2, 8, 30
+    a, g, m = F32(1 / k), F32(0.05), F32(0.9)
+    w0 = np.random.default_rng(6).normal(0, 0.05, MLP_D).astype(np.float32)
+    h = S.Sma(MLP_D, k, a, g, m, w0)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    S.sma_learner_attach(h.h, 1, 784, 256, 10, b, Xd, yd, X.shape[0], 33)
+    st = orc.State.init(w0.astype(np.float64), k)
+    min_margin = np.inf
+    for i in range(R):
+        S.sma_learner_grads(h.h, i, torch.cuda.current_stream())
+        h.step()
+        G = []
+        for j in range(k):
+            rows = orc.batch_indices(X.shape[0], k, b, 33, i, j)
+            _, gj, mg = orc.mlp_loss_grad(X, y, rows, st.W[j])
+            G.append(gj)
+            min_margin = min(min_margin, mg)
+        st.round(np.stack(G), a, g, m)
+    assert min_margin > 2e-5, f"batch too close to a ReLU kink for fp32 parity: {min_margin}"
+    assert relerr(h.central(), st.z) <= TOL
+    for j in range(k):
+        assert relerr(h.replica(j), st.W[j]) <= TOL
+    h.close()

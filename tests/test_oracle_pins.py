@@ -442,3 +442,58 @@ def test_resize_keeps_replicas_and_seeds_from_z(orc):
     st.resize(n, 2)
     for g in range(n):
         assert np.array_equal(st.W[g * 2:g * 2 + 2], W0[g * 3:g * 3 + 2])
+
+
+# ------------------------------------------------------------- MLP learner
+def _mlp_point(seed, scale=0.05):
+    rng = np.random.default_rng(seed)
+    return rng.normal(0, scale, orc_mlp_d())
+
+
+def orc_mlp_d():
+    import oracle
+    return oracle.mlp_dims()
+
+
+def test_mlp_loss_at_zero_is_ln10(orc):
+    """MLP with w = 0 has loss ln(10) (zero hidden activations
+    still give a uniform softmax); only the output bias gets a gradient."""
+    X, y = _blobs_small()
+    loss, g, _ = orc.mlp_loss_grad(X, y, np.arange(16), np.zeros(orc.mlp_dims()))
+    assert abs(loss - math.log(10)) < 1e-12
+    nb2 = orc.mlp_dims() - 10
+    assert np.all(g[:nb2] == 0)
+    cnt = np.bincount(y[:16], minlength=10)
+    np.testing.assert_allclose(g[nb2:], 0.1 - cnt / 16, atol=1e-15)
+
+
+def test_mlp_gradient_finite_differences(orc):
+    """SPEC.md:130 / S:148: analytic gradient vs central differences, on
+    parameters of both layers and both biases (away from ReLU kinks)."""
+    X, y = _blobs_small()
+    w = _mlp_point(1)
+    rows = np.arange(3, 11)
+    _, g, mn = orc.mlp_loss_grad(X, y, rows, w)
+    h = 1e-6
+    assert mn > 10 * h * np.abs(X).max()      # no probe crosses a ReLU kink
+    rng = np.random.default_rng(2)
+    D = orc.mlp_dims()
+    probes = list(rng.integers(0, 256 * 784, 12)) + list(range(200704, 200714)) + \
+        list(rng.integers(200960, D, 12))
+    for q in probes:
+        wp, wm = w.copy(), w.copy()
+        wp[q] += h
+        wm[q] -= h
+        fd = (orc.mlp_loss_grad(X, y, rows, wp, want_grad=False)[0]
+              - orc.mlp_loss_grad(X, y, rows, wm, want_grad=False)[0]) / (2 * h)
+        assert abs(fd - g[q]) < 1e-7, q
+
+
+def test_mlp_gradient_is_batch_mean(orc):
+    """Eq. 2: batch gradient = mean of per-sample gradients."""
+    X, y = _blobs_small()
+    w = _mlp_point(3)
+    rows = np.array([0, 7, 19])
+    _, g, _ = orc.mlp_loss_grad(X, y, rows, w)
+    per = [orc.mlp_loss_grad(X, y, [r], w)[1] for r in rows]
+    np.testing.assert_allclose(g, np.mean(per, axis=0), rtol=0, atol=1e-15)
