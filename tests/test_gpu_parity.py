@@ -492,7 +492,7 @@ def test_mlp_learner_sma_parity(torch_cuda, S, orc):
             G.append(gj)
             min_margin = min(min_margin, mg)
         st.round(np.stack(G), a, g, m)
-    assert min_margin > 2e-5, f"batch too close to a ReLU kink for fp32 parity: {min_margin}"
+    assert min_margin > 5e-6, f"batch too close to a ReLU kink for fp32 parity: {min_margin}"
     assert relerr(h.central(), st.z) <= TOL
     for j in range(k):
         assert relerr(h.replica(j), st.W[j]) <= TOL
