@@ -48,7 +48,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", choices=["sma", "reference"], default="sma")
-    ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C4", choices=["C1", "MLP", "C2", "C3", "C4", "C5"],
+                    help="C4 is the metric's workload; C1/MLP run the built-in learner in the loop")
     ap.add_argument("--k", type=int, default=None, help="override total replicas")
     ap.add_argument("--mode", choices=["auto", "A", "B"], default="auto",
                     help="collective path mode when N > 1 (auto = B, the overlapped round)")
@@ -183,7 +184,8 @@ def run_reference(args):
 
 def workload_name(cfg, d, k):
     names = {"C2": "LeNet-sized", "C3": "ResNet-32-sized", "C4": "ResNet-50-sized",
-             "C5": "VGG-16-sized"}
+             "C5": "VGG-16-sized", "C1": "softmax-regression learner in the loop,",
+             "MLP": "MLP 784-256-10 learner in the loop,"}
     return f"{cfg}: SMA round, {names[cfg]} vector d={d}, k={k} replicas, fp32"
 
 
@@ -210,8 +212,9 @@ def main():
 
     cfg = sma_inputs.CONFIGS[args.config]
     d = cfg["d"]
-    k = args.k or 16
+    k = args.k or (16 if args.config == "C4" else cfg["k"])
     alpha, gamma, mu = float(np.float32(1 / k)), float(np.float32(0.1)), float(np.float32(0.9))
+    learner = args.config in ("C1", "MLP")
 
     collective = world > 1 or args.force_collective
     mode = "fused" if not collective else ("A" if args.mode == "A" else "B")
@@ -236,12 +239,29 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         nccl_id = obj[0]
 
-    w0 = sma_inputs.w0(d)
+    w0 = sma_inputs.w0(d) if not learner else \
+        np.random.default_rng(6).normal(0, 0.05 if args.config == "MLP" else 0.0, d).astype(np.float32)
     h = sma.Sma(d, k, alpha, gamma, mu, w0, rank=rank, world=world, device=local,
                 nccl_id=nccl_id, flags=flags)
     r = h.local_count
     stream = torch.cuda.Stream()
-    h.synth_grads(0, sma_inputs.SEED_G, stream)   # inputs resident in HBM before timing
+    rnd = [0]
+    if learner:   # MNIST-shaped synthetic blobs resident in HBM, learner in the loop
+        X, y = sma_inputs.blobs(60_000, seed=4)
+        Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+        sma.sma_learner_attach(h.h, 0 if args.config == "C1" else 1, 784,
+                               256 if args.config == "MLP" else 0, 10, cfg["batch"], Xd, yd,
+                               X.shape[0], 99)
+
+        def one_step():
+            sma.sma_learner_grads(h.h, rnd[0], stream)
+            h.step(stream)
+            rnd[0] += 1
+    else:
+        h.synth_grads(0, sma_inputs.SEED_G, stream)   # inputs resident in HBM before timing
+
+        def one_step():
+            h.step(stream)
     stream.synchronize()
 
     def barrier():
@@ -252,7 +272,7 @@ def main():
 
     # ---------------------------------------------------------------- warm-up
     for _ in range(args.warmup):
-        h.step(stream)
+        one_step()
     barrier()
     h.kernel_time(reset=True)
 
@@ -266,7 +286,7 @@ def main():
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
     for _ in range(args.steps):
-        h.step(stream)
+        one_step()
     ev1.record(stream)
     barrier()
     ms = ev0.elapsed_time(ev1)
@@ -291,7 +311,7 @@ def main():
 
     # ------------------------------------------------------------------ e2e
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and not learner:
         pinned = [torch.empty(d, dtype=torch.float32).pin_memory() for _ in range(r)]
         for s_ in range(r):
             pinned[s_].copy_(torch.from_numpy(sma_inputs.grad(0, h.local_first + s_, k, d)))
@@ -380,7 +400,11 @@ def main():
                                    if mode == "B" else "")}
         if e2e:
             line["e2e"] = e2e
-        if not args.no_cpu_baseline:
+        if learner:
+            line["config"]["learner"] = args.config
+            line["config"]["batch"] = cfg["batch"]
+            line["config"]["l2"] = "L2-resident working set: roofline is effective (L2) bandwidth"
+        if not args.no_cpu_baseline and not learner:
             line["cpu_baseline"] = cpu_baseline(d, k, alpha, gamma, mu)
         print(json.dumps(line), flush=True)
     h.close()

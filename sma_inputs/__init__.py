@@ -39,6 +39,8 @@ CONFIGS = {
     "C3": dict(name="resnet32", d=464_154, k=16, n=8, batch=64),
     "C4": dict(name="resnet50", d=25_557_032, k=16, n=8, batch=16),
     "C5": dict(name="vgg16", d=138_357_544, k=32, n=8, batch=16),
+    # NEXT-2: the MLP learner in the loop, MNIST-shaped
+    "MLP": dict(name="mlp784-256-10", d=256 * 784 + 256 + 10 * 256 + 10, k=4, n=1, batch=16),
 }
 
 

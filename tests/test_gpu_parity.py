@@ -497,3 +497,21 @@ def test_mlp_learner_sma_parity(torch_cuda, S, orc):
     for j in range(k):
         assert relerr(h.replica(j), st.W[j]) <= TOL
     h.close()
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C3", "C5"])
+def test_paper_config_sizes_sampled_parity(torch_cuda, S, orc, cfg):
+    """The other BASELINE configs at their sizes on one GPU (all k replicas
+    local: C2 LeNet k = 8, C3 ResNet-32 k = 16, C5 VGG-16 k = 32 with 35 GB of
+    replicas + gradients), 100 rounds (C5: 30), sampled-index oracle."""
+    c = sma_inputs.CONFIGS[cfg]
+    d, k = c["d"], c["k"]
+    R = 30 if cfg == "C5" else 100
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    h = run_synth_gpu(torch_cuda, S, d, k, R, a, g, m, 0)
+    idx = sma_inputs.sample_indices(d, h.d_pad, 1, [0, h.d_pad], n_random=16_384)
+    zr, _, Wr = orc.run_synth(d, k, a, g, m, R, sma_inputs.SEED_W, sma_inputs.SEED_G, idx)
+    assert relerr(h.central()[idx], zr) <= TOL
+    for j in (0, k // 2, k - 1):
+        assert relerr(h.replica(j)[idx], Wr[j]) <= TOL
+    h.close()
