@@ -538,7 +538,6 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
   h->matc = (f & SMA_FLAG_MATERIALIZE_C) != 0;
   if ((f & SMA_FLAG_KERNEL_TMA) && (f & SMA_FLAG_KERNEL_LDG))
     return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_KERNEL_TMA and SMA_FLAG_KERNEL_LDG are exclusive");
-  h->tma = (f & SMA_FLAG_KERNEL_TMA) || (!(f & SMA_FLAG_KERNEL_LDG) && !h->collective);
   h->timing = (f & SMA_FLAG_TIMING) != 0;
   h->graphs = (f & SMA_FLAG_CUDA_GRAPH) != 0 && !h->timing;
   h->check = (f & SMA_FLAG_CHECK_FINITE) != 0;
@@ -549,6 +548,15 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
   h->n4 = h->d_pad / 4;
   STATUS_TRY(sma_plan_local_replicas(cfg->k, cfg->world, cfg->rank, &h->j0, &h->r));
   STATUS_TRY(sma_plan_shard_range(cfg->d, cfg->world, cfg->rank, &h->shard_off, &h->shard_len));
+  // Default kernel policy (measured, profiles/r01_sweep_small.jsonl): the TMA
+  // pipeline wins only on the fused path once a round streams well past L2
+  // (> 1 GiB); smaller rounds are latency/occupancy-bound and the 4-CTA/SM
+  // direct-load kernel is faster.
+  {
+    const double round_bytes = 4.0 * (double)h->d_pad * (3.0 * h->r + 3.0);
+    h->tma = (f & SMA_FLAG_KERNEL_TMA) ||
+             (!(f & SMA_FLAG_KERNEL_LDG) && !h->collective && round_bytes > 1073741824.0);
+  }
   if (h->r > SMA_MAX_LOCAL_REPLICAS)
     return fail(SMA_ERR_INVALID_ARG, "%d replicas on rank %d exceeds SMA_MAX_LOCAL_REPLICAS=%d",
                 h->r, cfg->rank, SMA_MAX_LOCAL_REPLICAS);

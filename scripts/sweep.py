@@ -12,7 +12,9 @@ steps = int(os.environ.get("SWEEP_STEPS", "300"))
 w0 = sma_inputs.w0(d)
 L, T = sma.FLAG_KERNEL_LDG, sma.FLAG_KERNEL_TMA
 if os.environ.get("SWEEP_TMA_ONLY"):
-    cases = [(16, T), (2, T), (32, T), (2, T | sma.FLAG_FORCE_COLLECTIVE)]
+    cases = [(16, T), (2, T), (8, T), (4, T), (2, T | sma.FLAG_FORCE_COLLECTIVE)]
+elif os.environ.get("SWEEP_LDG_ONLY"):
+    cases = [(16, L), (2, L), (8, L), (4, L), (2, L | sma.FLAG_FORCE_COLLECTIVE)]
 else:
     cases = [(16, L), (16, T), (2, L), (2, T),
              (2, sma.FLAG_FORCE_COLLECTIVE), (2, sma.FLAG_FORCE_COLLECTIVE | T),
