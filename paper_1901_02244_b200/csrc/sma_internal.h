@@ -66,14 +66,15 @@ cudaError_t launch_q_prologue(const float* W, int64_t ld, int r, const float* zp
 cudaError_t launch_synth_grads(float* G, int64_t ld, int r, int j0, int k, int64_t d,
                                int64_t round, uint64_t seed, int num_sms, cudaStream_t s);
 // Softmax-regression learner gradient for the r local replicas.
+// E: fp32 scratch [r][b][classes] (softmax minus one-hot).
 cudaError_t launch_softmax_grad(const float* X, const int32_t* y, const int32_t* perm,
                                 int64_t pos0, int b, int in_dim, int classes, const float* W,
-                                int64_t ld, int r, int j0, float* G, cudaStream_t s);
+                                int64_t ld, int r, int j0, float* E, float* G, cudaStream_t s);
 // MLP learner (kind 1) gradient for the r local replicas (sma_learner_mlp.cu).
-// A1: fp64 scratch [r][b][hidden]; DA: fp32 scratch [r][b][hidden].
+// A1: double-float scratch [r][b][hidden]; DA: fp32 scratch [r][b][hidden].
 cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* perm, int64_t pos0,
                             int b, int in_dim, int hidden, int classes, const float* W, int64_t ld,
-                            int r, int j0, double* A1, float* DA, float* G, cudaStream_t s);
+                            int r, int j0, float2* A1, float* DA, float* G, cudaStream_t s);
 // Broadcast: dst rows [r][ld] := src [ld]   and   y := x   (restart / init).
 cudaError_t launch_broadcast_rows(float* dst, int64_t ld, int r, const float* src, int64_t n4,
                                   int num_sms, cudaStream_t s);

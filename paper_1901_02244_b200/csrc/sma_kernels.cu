@@ -330,70 +330,99 @@ __global__ void __launch_bounds__(kThreads) synth_grads_kernel(float* __restrict
 }
 
 // ------------------------------------------------ softmax learner (a2')
-// grid (r, kSoftmaxSplit): every CTA of learner `slot` gathers the b rows of
-// its batch into shared memory, computes the b x classes logits (one warp per
-// (row, class) pair, lanes stride the features, xor-shuffle reduction), the
-// max-subtracted softmax and e = p - onehot(y); then it writes the slice
-// blockIdx.y of dW[c][f] = (1/b) sum_t e[t][c] x[t][f] (and db on slice 0).
+// Two kernels, both spread over many SMs (one CTA per learner was bound by
+// instruction issue on r SMs: 21 us; profiles/r01_ncu_learners.txt):
+//  softmax_logits_kernel  grid (r, b), one warp per class: logits of row t,
+//      max-subtracted softmax, E[slot][t][c] = p - onehot(y_t)   (fp32)
+//  softmax_wgrad_kernel   grid (r, ceil(in_dim / kFeat)): for a slice of
+//      kFeat features, dW[c][f] = (1/b) sum_t E[t][c] x[t][f]; db on slice 0.
 // fp32 FFMA throughout (no TF32: SURVEY Appendix A5).
-constexpr int kSoftmaxSplit = 8;
-constexpr int kSoftmaxThreads = 512;
-__global__ void __launch_bounds__(kSoftmaxThreads) softmax_grad_kernel(
+constexpr int kFeat = 64;
+constexpr int kMaxClasses = 32;
+
+__global__ void __launch_bounds__(kMaxClasses * 32) softmax_logits_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ y, const int32_t* __restrict__ perm,
     int64_t pos0, int b, int in_dim, int classes, const float* __restrict__ Wall, int64_t ld,
-    int j0, float* __restrict__ Gall) {
-  extern __shared__ float smem[];
-  float* xs = smem;                          // [b][in_dim]
-  float* e = xs + (int64_t)b * in_dim;       // [b][classes]
-  int* rows = (int*)(e + b * classes);       // [b]
-  const int slot = blockIdx.x;
+    int j0, float* __restrict__ E) {
+  extern __shared__ __align__(16) float xs[];  // [in_dim]
+  __shared__ float lg[kMaxClasses];
+  const int slot = blockIdx.x, t = blockIdx.y;
+  const int row = perm[pos0 + (int64_t)(j0 + slot) * b + t];
+  const float* x = X + (int64_t)row * in_dim;
   const float* W = Wall + (int64_t)slot * ld;
-  float* G = Gall + (int64_t)slot * ld;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  if (threadIdx.x < b) rows[threadIdx.x] = perm[pos0 + (int64_t)(j0 + slot) * b + threadIdx.x];
-  __syncthreads();
-  for (int q = threadIdx.x; q < b * in_dim; q += blockDim.x) {
-    const int t = q / in_dim, f = q - t * in_dim;
-    xs[q] = X[(int64_t)rows[t] * in_dim + f];
+  const bool vec = (in_dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
+  if (vec) {
+    for (int q = threadIdx.x; q < (in_dim >> 2); q += blockDim.x)
+      reinterpret_cast<float4*>(xs)[q] = __ldg(reinterpret_cast<const float4*>(x) + q);
+  } else {
+    for (int q = threadIdx.x; q < in_dim; q += blockDim.x) xs[q] = x[q];
   }
   __syncthreads();
-  const float* bias = W + (int64_t)classes * in_dim;
-  for (int pr = warp; pr < b * classes; pr += nwarps) {
-    const int t = pr / classes, c = pr - t * classes;
+  const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
+  if (c < classes) {  // warp c: logit of class c, W row c read straight from L2
+    const float* w = W + (int64_t)c * in_dim;
     float s = 0.f;
-    for (int f = lane; f < in_dim; f += 32) s = __fmaf_rn(W[(int64_t)c * in_dim + f], xs[t * in_dim + f], s);
+    if (vec) {
+      const float4* w4 = reinterpret_cast<const float4*>(w);
+      const float4* x4 = reinterpret_cast<const float4*>(xs);
+#pragma unroll 4
+      for (int f = lane; f < (in_dim >> 2); f += 32) {
+        const float4 a = __ldg(w4 + f), v = x4[f];
+        s = __fmaf_rn(a.x, v.x, s);
+        s = __fmaf_rn(a.y, v.y, s);
+        s = __fmaf_rn(a.z, v.z, s);
+        s = __fmaf_rn(a.w, v.w, s);
+      }
+    } else {
+      for (int f = lane; f < in_dim; f += 32) s = __fmaf_rn(w[f], xs[f], s);
+    }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
-    if (lane == 0) e[pr] = __fadd_rn(s, bias[c]);
+    if (lane == 0) lg[c] = __fadd_rn(s, W[(int64_t)classes * in_dim + c]);
   }
   __syncthreads();
-  if (threadIdx.x < b) {  // softmax of row t, then e = p - onehot(y_t)
-    const int t = threadIdx.x;
-    float mx = e[t * classes];
-    for (int c = 1; c < classes; ++c) mx = fmaxf(mx, e[t * classes + c]);
+  if (threadIdx.x == 0) {  // max-subtracted softmax of this row, e = p - onehot(y_t)
+    float mx = lg[0];
+    for (int k = 1; k < classes; ++k) mx = fmaxf(mx, lg[k]);
     float den = 0.f;
-    for (int c = 0; c < classes; ++c) den = __fadd_rn(den, expf(__fsub_rn(e[t * classes + c], mx)));
-    const int yt = y[rows[t]];
-    for (int c = 0; c < classes; ++c) {
-      const float pc = __fdiv_rn(expf(__fsub_rn(e[t * classes + c], mx)), den);
-      e[t * classes + c] = __fsub_rn(pc, c == yt ? 1.f : 0.f);
-    }
+    for (int k = 0; k < classes; ++k) den = __fadd_rn(den, expf(__fsub_rn(lg[k], mx)));
+    const int yt = y[row];
+    float* e = E + ((int64_t)slot * b + t) * classes;
+    for (int k = 0; k < classes; ++k)
+      e[k] = __fsub_rn(__fdiv_rn(expf(__fsub_rn(lg[k], mx)), den), k == yt ? 1.f : 0.f);
+  }
+}
+
+__global__ void __launch_bounds__(256) softmax_wgrad_kernel(
+    const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
+    int classes, int j0, int64_t ld, const float* __restrict__ E, float* __restrict__ Gall) {
+  extern __shared__ float sm[];
+  float* xs = sm;                  // [b][kFeat]
+  float* e = xs + b * kFeat;       // [b][classes]
+  __shared__ int rows[64];
+  const int slot = blockIdx.x, f0 = blockIdx.y * kFeat;
+  const int nf = min(kFeat, in_dim - f0);
+  float* G = Gall + (int64_t)slot * ld;
+  if (threadIdx.x < b) rows[threadIdx.x] = perm[pos0 + (int64_t)(j0 + slot) * b + threadIdx.x];
+  for (int q = threadIdx.x; q < b * classes; q += blockDim.x) e[q] = E[(int64_t)slot * b * classes + q];
+  __syncthreads();
+  for (int q = threadIdx.x; q < b * kFeat; q += blockDim.x) {
+    const int t = q / kFeat, f = q - t * kFeat;
+    xs[q] = f < nf ? __ldg(X + (int64_t)rows[t] * in_dim + f0 + f) : 0.f;
   }
   __syncthreads();
   const float fb = (float)b;
-  const int nW = classes * in_dim;
-  const int per = (nW + gridDim.y - 1) / gridDim.y;
-  const int lo = blockIdx.y * per, hi = min(nW, lo + per);
-  for (int q = lo + threadIdx.x; q < hi; q += blockDim.x) {
-    const int c = q / in_dim, f = q - c * in_dim;
+  for (int q = threadIdx.x; q < classes * kFeat; q += blockDim.x) {
+    const int c = q / kFeat, f = q - c * kFeat;
+    if (f >= nf) continue;
     float s = 0.f;
-    for (int t = 0; t < b; ++t) s = __fmaf_rn(e[t * classes + c], xs[t * in_dim + f], s);
-    G[q] = __fdiv_rn(s, fb);
+    for (int t = 0; t < b; ++t) s = __fmaf_rn(e[t * classes + c], xs[t * kFeat + f], s);
+    G[(int64_t)c * in_dim + f0 + f] = __fdiv_rn(s, fb);
   }
   if (blockIdx.y == 0 && threadIdx.x < classes) {
     float s = 0.f;
     for (int t = 0; t < b; ++t) s = __fadd_rn(s, e[t * classes + threadIdx.x]);
-    G[nW + threadIdx.x] = __fdiv_rn(s, fb);
+    G[(int64_t)classes * in_dim + threadIdx.x] = __fdiv_rn(s, fb);
   }
 }
 
@@ -514,14 +543,17 @@ cudaError_t launch_synth_grads(float* G, int64_t ld, int r, int j0, int k, int64
 
 cudaError_t launch_softmax_grad(const float* X, const int32_t* y, const int32_t* perm, int64_t pos0,
                                 int b, int in_dim, int classes, const float* W, int64_t ld, int r,
-                                int j0, float* G, cudaStream_t s) {
-  const size_t smem = sizeof(float) * ((size_t)b * in_dim + (size_t)b * classes) + sizeof(int) * b;
-  cudaError_t e = cudaFuncSetAttribute(softmax_grad_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                                int j0, float* E, float* G, cudaStream_t s) {
+  if (classes > kMaxClasses || b > 64) return cudaErrorInvalidValue;
+  const size_t sm1 = sizeof(float) * (size_t)in_dim;
+  const size_t sm2 = sizeof(float) * ((size_t)b * kFeat + (size_t)b * classes);
+  cudaError_t e = cudaFuncSetAttribute(softmax_logits_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
   if (e != cudaSuccess) return e;
-  dim3 grid(r, kSoftmaxSplit);
-  softmax_grad_kernel<<<grid, kSoftmaxThreads, smem, s>>>(X, y, perm, pos0, b, in_dim, classes, W,
-                                                          ld, j0, G);
+  softmax_logits_kernel<<<dim3(r, b), classes * 32, sm1, s>>>(X, y, perm, pos0, b, in_dim, classes, W,
+                                                              ld, j0, E);
+  softmax_wgrad_kernel<<<dim3(r, (in_dim + kFeat - 1) / kFeat), 256, sm2, s>>>(
+      X, perm, pos0, b, in_dim, classes, j0, ld, E, G);
   return cudaGetLastError();
 }
 

@@ -253,7 +253,7 @@ struct sma_handle {
   // learner
   bool learner = false;
   int kind = 0, in_dim = 0, hidden = 0, classes = 0, batch = 0;
-  double* mlp_A1 = nullptr;  // MLP scratch, sized for SMA_MAX_LOCAL_REPLICAS learners
+  float2* mlp_A1 = nullptr;  // MLP scratch, sized for SMA_MAX_LOCAL_REPLICAS learners
   float* mlp_DA = nullptr;
   const float* X = nullptr;
   const int32_t* y = nullptr;
@@ -511,7 +511,8 @@ sma_status alloc_zero(float** p, size_t n) {
 // SMA_NCCL_MEMALLOC != 0), else cudaMalloc.  Zero-filled.
 sma_status alloc_coll(sma_handle* h, float** p, size_t n) {
   const char* e = getenv("SMA_NCCL_MEMALLOC");
-  const bool use = g_nccl.MemAlloc && g_nccl.MemFree && !(e && e[0] == '0');
+  // a 1-rank communicator gains nothing from registration (no NVLS team)
+  const bool use = h->cfg.world > 1 && g_nccl.MemAlloc && g_nccl.MemFree && !(e && e[0] == '0');
   if (!use) return alloc_zero(p, n);
   void* q = nullptr;
   NCCL_TRY(g_nccl.MemAlloc(&q, sizeof(float) * n));
@@ -993,7 +994,7 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
   if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
   if (kind != 0 && kind != 1)
     return fail(SMA_ERR_INVALID_ARG, "learner kind %d not available (0 softmax, 1 mlp)", kind);
-  if (in_dim < 1 || classes < 2 || batch < 1 || batch > 64 || !X_dev || !y_dev ||
+  if (in_dim < 1 || classes < 2 || classes > 32 || batch < 1 || batch > 64 || !X_dev || !y_dev ||
       (kind == 1 && (hidden < 1 || hidden > 4096)))
     return fail(SMA_ERR_INVALID_ARG, "bad learner arguments");
   const int64_t dl = kind == 0 ? (int64_t)classes * in_dim + classes
@@ -1003,9 +1004,11 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
                 (long long)h->cfg.d, (long long)dl);
   if (n_samples < (int64_t)h->cfg.k * batch || n_samples > INT32_MAX)
     return fail(SMA_ERR_INVALID_ARG, "n_samples must be in [k*batch, 2^31)");
-  if ((size_t)batch * in_dim * sizeof(float) > 200 * 1024 ||
-      (kind == 1 && (size_t)batch * (hidden + classes) * sizeof(float) > 200 * 1024))
-    return fail(SMA_ERR_INVALID_ARG, "batch too large for shared memory");
+  const size_t smem_need =
+      kind == 0 ? sizeof(float) * ((size_t)in_dim + (size_t)batch * (64 + classes))
+                : sizeof(float) * ((size_t)(batch + 16) * in_dim);
+  if (smem_need > 200 * 1024)
+    return fail(SMA_ERR_INVALID_ARG, "batch/in_dim too large for the learner's shared memory");
   DeviceGuard guard(h->dev);
   STATUS_TRY(sync_handle(h));
   for (int i = 0; i < 2; ++i) {
@@ -1018,13 +1021,13 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
   h->perm_host = nullptr;
   CUDA_TRY(cudaMallocHost(&h->perm_host, sizeof(int32_t) * (size_t)n_samples));
   STATUS_TRY(ensure_G(h));
-  if (kind == 1) {
+  {  // learner scratch, sized for SMA_MAX_LOCAL_REPLICAS learners (resize-safe)
     cudaFree(h->mlp_A1);
     cudaFree(h->mlp_DA);
     h->mlp_A1 = nullptr;
     h->mlp_DA = nullptr;
-    const size_t n = (size_t)SMA_MAX_LOCAL_REPLICAS * batch * hidden;
-    CUDA_TRY(cudaMalloc(&h->mlp_A1, sizeof(double) * n));
+    const size_t n = (size_t)SMA_MAX_LOCAL_REPLICAS * batch * (kind == 1 ? hidden : classes);
+    if (kind == 1) CUDA_TRY(cudaMalloc(&h->mlp_A1, sizeof(float2) * n));
     CUDA_TRY(cudaMalloc(&h->mlp_DA, sizeof(float) * n));
   }
   h->learner = true;
@@ -1063,8 +1066,8 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
   const int64_t pos0 = (round % E) * h->cfg.k * (int64_t)h->batch;
   if (h->kind == 0) {
     CUDA_TRY(launch_softmax_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim,
-                                 h->classes, h->W, h->d_pad, h->r, h->j0, h->G, s));
-    ++h->launches;
+                                 h->classes, h->W, h->d_pad, h->r, h->j0, h->mlp_DA, h->G, s));
+    h->launches += 2;
   } else {
     CUDA_TRY(launch_mlp_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim, h->hidden,
                              h->classes, h->W, h->d_pad, h->r, h->j0, h->mlp_A1, h->mlp_DA, h->G, s));
