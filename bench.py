@@ -279,7 +279,8 @@ def main():
     for _ in range(args.warmup):
         one_step()
     barrier()
-    h.kernel_time(reset=True)
+    for ph in range(5):
+        h.kernel_time(reset=True, phase=ph)
 
     # ------------------------------------------------------------ timed region
     clocks = ClockSampler(local)
