@@ -258,9 +258,8 @@ def main():
                                256 if args.config == "MLP" else 0, 10, cfg["batch"], Xd, yd,
                                X.shape[0], 99)
 
-        def one_step():
-            sma.sma_learner_grads(h.h, rnd[0], stream)
-            h.step(stream)
+        def one_step():   # learner gradient + round (fused for the softmax learner)
+            sma.sma_learner_step(h.h, rnd[0], stream)
             rnd[0] += 1
     else:
         h.synth_grads(0, sma_inputs.SEED_G, stream)   # inputs resident in HBM before timing

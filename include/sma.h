@@ -269,6 +269,14 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
  * cuda_stream.  Errors: STATE (no learner attached), CUDA. */
 sma_status sma_learner_grads(sma_handle* h, int64_t round, void* cuda_stream);
 
+/* One full round with the learner in the loop: exactly sma_learner_grads then
+ * sma_step (same results), but for the softmax learner on a single-GPU handle
+ * (no MATERIALIZE_C, no CUDA graph) the gradient slice, the replica update and
+ * the central update run fused in one kernel after the logits kernel, so the
+ * gradient never makes an HBM round trip (the gradient buffers are still
+ * written and registered).  Errors: as sma_learner_grads and sma_step. */
+sma_status sma_learner_step(sma_handle* h, int64_t round, void* cuda_stream);
+
 /* ------------------------------------------------ bookkeeping (host only) */
 /* Pure functions of their arguments; no device, no handle (bit-exact with
  * the oracle's independent implementation). */

@@ -70,6 +70,12 @@ cudaError_t launch_synth_grads(float* G, int64_t ld, int r, int j0, int k, int64
 cudaError_t launch_softmax_grad(const float* X, const int32_t* y, const int32_t* perm,
                                 int64_t pos0, int b, int in_dim, int classes, const float* W,
                                 int64_t ld, int r, int j0, float* E, float* G, cudaStream_t s);
+// Softmax learner + the fused n = 1 round in two kernels (logits, then
+// gradient slice + replica update + central update); bitwise equal to
+// launch_softmax_grad followed by replica_step_ldg<kFused>.
+cudaError_t launch_softmax_round(const float* X, const int32_t* y, const int32_t* perm,
+                                 int64_t pos0, int b, int in_dim, int classes, int j0, float* E,
+                                 float* G, const ReplicaArgs& a, cudaStream_t s);
 // MLP learner (kind 1) gradient for the r local replicas (sma_learner_mlp.cu).
 // A1: double-float scratch [r][b][hidden]; DA: fp32 scratch [r][b][hidden].
 cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* perm, int64_t pos0,

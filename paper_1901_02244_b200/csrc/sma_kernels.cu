@@ -426,6 +426,89 @@ __global__ void __launch_bounds__(256) softmax_wgrad_kernel(
   }
 }
 
+// Learner-fused round (n = 1, softmax learner): the dW slice computation of
+// softmax_wgrad_kernel followed directly by a3-a5 + a7 for the same parameters
+// of ALL r replicas, so the gradient never makes an HBM round trip and the
+// round needs no separate replica kernel.  CTA x < nfs owns features
+// [64x, 64x + 64) of every class; CTA nfs owns the biases.  The arithmetic per
+// element is exactly that of softmax_wgrad_kernel then replica_step_ldg<kFused>
+// (same operation order), so the result is bitwise identical to the unfused
+// pair.  The gradient is still written to G (the registered buffers).
+constexpr int kFusedPerThread = 3;  // ceil(classes * kFeat / 256) for classes <= 12
+__global__ void __launch_bounds__(256) softmax_round_kernel(
+    const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
+    int classes, int j0, const float* __restrict__ E, float* __restrict__ Gall, const ReplicaArgs a) {
+  extern __shared__ float sm[];
+  float* xs = sm;                  // [b][kFeat]
+  float* e = xs + b * kFeat;       // [b][classes]
+  __shared__ int rows[64];
+  const int nfs = (in_dim + kFeat - 1) / kFeat;
+  const bool bias = blockIdx.x == nfs;
+  const int f0 = blockIdx.x * kFeat;
+  const int nf = bias ? 0 : min(kFeat, in_dim - f0);
+  const int nparam = bias ? classes : classes * kFeat;
+  int64_t pidx[kFusedPerThread];
+  float z[kFusedPerThread], acc[kFusedPerThread];
+#pragma unroll
+  for (int u = 0; u < kFusedPerThread; ++u) {
+    const int q = threadIdx.x + u * 256;
+    pidx[u] = -1;
+    acc[u] = 0.f;
+    z[u] = 0.f;
+    if (q < nparam) {
+      if (bias) {
+        pidx[u] = (int64_t)classes * in_dim + q;
+      } else {
+        const int c = q / kFeat, f = q - c * kFeat;
+        if (f < nf) pidx[u] = (int64_t)c * in_dim + f0 + f;
+      }
+      if (pidx[u] >= 0) z[u] = a.z[pidx[u]];
+    }
+  }
+  const float fb = (float)b;
+  bool bad = false;
+  for (int j = 0; j < a.r; ++j) {
+    __syncthreads();  // previous learner's tiles are consumed
+    if (threadIdx.x < b) rows[threadIdx.x] = perm[pos0 + (int64_t)(j0 + j) * b + threadIdx.x];
+    for (int q = threadIdx.x; q < b * classes; q += blockDim.x) e[q] = E[(int64_t)j * b * classes + q];
+    __syncthreads();
+    if (!bias)
+      for (int q = threadIdx.x; q < b * kFeat; q += blockDim.x) {
+        const int t = q / kFeat, f = q - t * kFeat;
+        xs[q] = f < nf ? __ldg(X + (int64_t)rows[t] * in_dim + f0 + f) : 0.f;
+      }
+    __syncthreads();
+    float* W = a.W + (int64_t)j * a.ld;
+    float* G = Gall + (int64_t)j * a.ld;
+#pragma unroll
+    for (int u = 0; u < kFusedPerThread; ++u) {
+      if (pidx[u] < 0) continue;
+      const int q = threadIdx.x + u * 256;
+      float s = 0.f;
+      if (bias) {
+        for (int t = 0; t < b; ++t) s = __fadd_rn(s, e[t * classes + q]);
+      } else {
+        const int c = q / kFeat, f = q - c * kFeat;
+        for (int t = 0; t < b; ++t) s = __fmaf_rn(e[t * classes + c], xs[t * kFeat + f], s);
+      }
+      const float g = __fdiv_rn(s, fb);
+      G[pidx[u]] = g;
+      const StepOut o = sma_elem(W[pidx[u]], g, z[u], a.alpha, a.gamma);
+      W[pidx[u]] = o.wn;
+      acc[u] = __fadd_rn(acc[u], o.c);
+      bad |= !isfinite(o.wn);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kFusedPerThread; ++u) {
+    if (pidx[u] < 0) continue;
+    const float zn = central_elem(z[u], acc[u], a.zprev_next[pidx[u]], a.mu);
+    a.zprev_next[pidx[u]] = zn;
+    bad |= !isfinite(zn);
+  }
+  if (a.nonfinite && bad) atomicOr(a.nonfinite, 1);
+}
+
 __global__ void __launch_bounds__(kThreads) broadcast_rows_kernel(float* __restrict__ dst, int64_t ld,
                                                                   int r, const float* __restrict__ src,
                                                                   int64_t n4) {
@@ -554,6 +637,23 @@ cudaError_t launch_softmax_grad(const float* X, const int32_t* y, const int32_t*
                                                               ld, j0, E);
   softmax_wgrad_kernel<<<dim3(r, (in_dim + kFeat - 1) / kFeat), 256, sm2, s>>>(
       X, perm, pos0, b, in_dim, classes, j0, ld, E, G);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_softmax_round(const float* X, const int32_t* y, const int32_t* perm,
+                                 int64_t pos0, int b, int in_dim, int classes, int j0, float* E,
+                                 float* G, const ReplicaArgs& a, cudaStream_t s) {
+  if (classes > kMaxClasses || b > 64 || classes * kFeat > kFusedPerThread * 256)
+    return cudaErrorInvalidValue;
+  const size_t sm1 = sizeof(float) * (size_t)in_dim;
+  const size_t sm2 = sizeof(float) * ((size_t)b * kFeat + (size_t)b * classes);
+  cudaError_t e = cudaFuncSetAttribute(softmax_logits_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+  if (e != cudaSuccess) return e;
+  softmax_logits_kernel<<<dim3(a.r, b), classes * 32, sm1, s>>>(X, y, perm, pos0, b, in_dim, classes,
+                                                                a.W, a.ld, j0, E);
+  const int nfs = (in_dim + kFeat - 1) / kFeat;
+  softmax_round_kernel<<<nfs + 1, 256, sm2, s>>>(X, perm, pos0, b, in_dim, classes, j0, E, G, a);
   return cudaGetLastError();
 }
 

@@ -1043,19 +1043,14 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
   return SMA_OK;
 }
 
-sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
-  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
-  if (!h->learner) return fail(SMA_ERR_STATE, "no learner attached");
-  if (round < 0) return fail(SMA_ERR_INVALID_ARG, "round < 0");
-  if (h->r == 0) return SMA_OK;
-  DeviceGuard guard(h->dev);
-  cudaStream_t s = (cudaStream_t)stream;
+// The batch permutation of `round`'s epoch on the device (R10): built on the
+// host and uploaded when the epoch changes (double-buffered by epoch parity).
+static sma_status learner_batch(sma_handle* h, int64_t round, cudaStream_t s, int* buf_out,
+                         int64_t* pos0_out) {
   const int64_t E = h->n_samples / ((int64_t)h->cfg.k * h->batch);
   const int64_t e = round / E;
   const int buf = (int)(e & 1);
   if (h->perm_epoch[buf] != e) {
-    // new epoch: build pi_e on the host (R10) and upload it; the pinned
-    // staging buffer is reused only after the previous upload completed.
     STATUS_TRY(sync_handle(h));
     plan_epoch_permutation(h->n_samples, h->batch_seed, e, h->perm_host);
     CUDA_TRY(cudaMemcpyAsync(h->perm_dev[buf], h->perm_host, sizeof(int32_t) * h->n_samples,
@@ -1063,7 +1058,21 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
     CUDA_TRY(cudaStreamSynchronize(s));
     h->perm_epoch[buf] = e;
   }
-  const int64_t pos0 = (round % E) * h->cfg.k * (int64_t)h->batch;
+  *buf_out = buf;
+  *pos0_out = (round % E) * h->cfg.k * (int64_t)h->batch;
+  return SMA_OK;
+}
+
+sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (!h->learner) return fail(SMA_ERR_STATE, "no learner attached");
+  if (round < 0) return fail(SMA_ERR_INVALID_ARG, "round < 0");
+  if (h->r == 0) return SMA_OK;
+  DeviceGuard guard(h->dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  int buf = 0;
+  int64_t pos0 = 0;
+  STATUS_TRY(learner_batch(h, round, s, &buf, &pos0));
   if (h->kind == 0) {
     CUDA_TRY(launch_softmax_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim,
                                  h->classes, h->W, h->d_pad, h->r, h->j0, h->mlp_DA, h->G, s));
@@ -1074,6 +1083,45 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
     h->launches += 3;
   }
   for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
+  return mark_done(h, s);
+}
+
+sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (!h->learner) return fail(SMA_ERR_STATE, "no learner attached");
+  if (round < 0) return fail(SMA_ERR_INVALID_ARG, "round < 0");
+  const bool fusable = h->kind == 0 && !h->collective && !h->matc && h->r > 0 &&
+                       h->classes * 64 <= 3 * 256 && !h->graphs;
+  if (!fusable) {  // the same result through the two public calls
+    STATUS_TRY(sma_learner_grads(h, round, stream));
+    return sma_step(h, stream);
+  }
+  DeviceGuard guard(h->dev);
+  cudaStream_t s = (cudaStream_t)stream;
+  int buf = 0;
+  int64_t pos0 = 0;
+  STATUS_TRY(learner_batch(h, round, s, &buf, &pos0));
+  ReplicaArgs a{};
+  a.W = h->W;
+  a.ld = h->d_pad;
+  a.r = h->r;
+  a.d = h->cfg.d;
+  a.n4 = h->n4;
+  a.z = h->z();
+  a.zprev_next = h->zprev();
+  a.alpha = h->alpha;
+  a.gamma = h->gamma;
+  a.mu = h->mu;
+  a.nonfinite = h->check ? h->nonfinite : nullptr;
+  cudaEvent_t* tp = nullptr;
+  STATUS_TRY(timer_pair(h, SMA_PHASE_REPLICA, &tp));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
+  CUDA_TRY(launch_softmax_round(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim,
+                                h->classes, h->j0, h->mlp_DA, h->G, a, s));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
+  h->launches += 2;
+  for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
+  advance(h);
   return mark_done(h, s);
 }
 

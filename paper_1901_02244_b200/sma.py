@@ -41,7 +41,7 @@ EXPORTS = ["sma_create", "sma_destroy", "sma_set_learner_grads", "sma_set_learne
            "sma_plan_replica_location", "sma_plan_local_replicas", "sma_plan_shard_range",
            "sma_plan_batch_indices", "sma_nccl_unique_id", "sma_kernel_time",
            "sma_launch_count", "sma_info", "sma_last_error", "sma_abi_version",
-           "sma_step_local", "sma_autotune_step", "sma_set_local_replicas"]
+           "sma_step_local", "sma_autotune_step", "sma_set_local_replicas", "sma_learner_step"]
 
 
 class SmaError(RuntimeError):
@@ -103,6 +103,7 @@ def load():
         "sma_step_local": ([P, P], st),
         "sma_autotune_step": ([i32, C.c_double, P, P, P], st),
         "sma_set_local_replicas": ([P, i32, P], st),
+        "sma_learner_step": ([P, i64, P], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -236,6 +237,10 @@ def sma_learner_attach(h: int, kind: int, in_dim: int, hidden: int, classes: int
 
 def sma_learner_grads(h: int, rnd: int, stream=None) -> None:
     _check(load().sma_learner_grads(h, rnd, _stream(stream)), "sma_learner_grads")
+
+
+def sma_learner_step(h: int, rnd: int, stream=None) -> None:
+    _check(load().sma_learner_step(h, rnd, _stream(stream)), "sma_learner_step")
 
 
 def sma_plan_d_pad(d: int, world: int) -> int:

@@ -515,3 +515,34 @@ def test_paper_config_sizes_sampled_parity(torch_cuda, S, orc, cfg):
     for j in (0, k // 2, k - 1):
         assert relerr(h.replica(j)[idx], Wr[j]) <= TOL
     h.close()
+
+
+def test_learner_step_fused_is_bitwise_unfused(torch_cuda, S, orc):
+    """sma_learner_step's fused softmax round == sma_learner_grads + sma_step,
+    bit for bit (same per-element operation order), over 60 rounds crossing an
+    epoch; and both match the oracle (config C1 shape)."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(3_000, seed=4)
+    k, b, R = 4, 16, 60
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    hs = []
+    for fused in (True, False):
+        h = S.Sma(7850, k, a, g, m, np.zeros(7850, np.float32))
+        S.sma_learner_attach(h.h, 0, 784, 0, 10, b, Xd, yd, X.shape[0], 99)
+        s = torch.cuda.Stream()
+        for i in range(R):
+            if fused:
+                S.sma_learner_step(h.h, i, s)
+            else:
+                S.sma_learner_grads(h.h, i, s)
+                h.step(s)
+        hs.append(h)
+    assert np.array_equal(hs[0].central(), hs[1].central())
+    assert np.array_equal(hs[0].central_prev(), hs[1].central_prev())
+    for j in range(k):
+        assert np.array_equal(hs[0].replica(j), hs[1].replica(j))
+    zr, _, _ = orc.run_softmax(X, y, b, 99, k, a, g, m, R, np.zeros(7850))
+    assert relerr(hs[0].central(), zr) <= TOL
+    for h in hs:
+        h.close()
