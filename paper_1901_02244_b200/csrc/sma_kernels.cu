@@ -430,80 +430,76 @@ __global__ void __launch_bounds__(256) softmax_wgrad_kernel(
 // softmax_wgrad_kernel followed directly by a3-a5 + a7 for the same parameters
 // of ALL r replicas, so the gradient never makes an HBM round trip and the
 // round needs no separate replica kernel.  CTA x < nfs owns features
-// [64x, 64x + 64) of every class; CTA nfs owns the biases.  The arithmetic per
-// element is exactly that of softmax_wgrad_kernel then replica_step_ldg<kFused>
-// (same operation order), so the result is bitwise identical to the unfused
-// pair.  The gradient is still written to G (the registered buffers).
-constexpr int kFusedPerThread = 3;  // ceil(classes * kFeat / 256) for classes <= 12
+// [32x, 32x + 32) of every class; CTA nfs owns the biases.  All r learners'
+// batch tiles are staged at once; each thread then walks its parameters and,
+// per parameter, the learners in ascending j (4 replica loads in flight).  The
+// arithmetic per element is exactly that of softmax_wgrad_kernel then
+// replica_step_ldg<kFused> (same operation order), so the result is bitwise
+// identical to the unfused pair.  The gradient is still written to G.
+constexpr int kFeatF = 32;
+constexpr int kFusedPerThread = 2;  // ceil(classes * kFeatF / 256) for classes <= 16
 __global__ void __launch_bounds__(256) softmax_round_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
     int classes, int j0, const float* __restrict__ E, float* __restrict__ Gall, const ReplicaArgs a) {
   extern __shared__ float sm[];
-  float* xs = sm;                  // [b][kFeat]
-  float* e = xs + b * kFeat;       // [b][classes]
-  __shared__ int rows[64];
-  const int nfs = (in_dim + kFeat - 1) / kFeat;
+  const int r = a.r;
+  float* xs = sm;                              // [r][b][kFeatF]
+  float* e = xs + (int64_t)r * b * kFeatF;     // [r][b][classes]
+  int* rows = (int*)(e + (int64_t)r * b * classes);  // [r][b]
+  const int nfs = (in_dim + kFeatF - 1) / kFeatF;
   const bool bias = blockIdx.x == nfs;
-  const int f0 = blockIdx.x * kFeat;
-  const int nf = bias ? 0 : min(kFeat, in_dim - f0);
-  const int nparam = bias ? classes : classes * kFeat;
-  int64_t pidx[kFusedPerThread];
-  float z[kFusedPerThread], acc[kFusedPerThread];
-#pragma unroll
-  for (int u = 0; u < kFusedPerThread; ++u) {
-    const int q = threadIdx.x + u * 256;
-    pidx[u] = -1;
-    acc[u] = 0.f;
-    z[u] = 0.f;
-    if (q < nparam) {
-      if (bias) {
-        pidx[u] = (int64_t)classes * in_dim + q;
-      } else {
-        const int c = q / kFeat, f = q - c * kFeat;
-        if (f < nf) pidx[u] = (int64_t)c * in_dim + f0 + f;
-      }
-      if (pidx[u] >= 0) z[u] = a.z[pidx[u]];
-    }
+  const int f0 = blockIdx.x * kFeatF;
+  const int nf = bias ? 0 : min(kFeatF, in_dim - f0);
+  for (int q = threadIdx.x; q < r * b; q += blockDim.x) {
+    const int j = q / b, t = q - j * b;
+    rows[q] = perm[pos0 + (int64_t)(j0 + j) * b + t];
   }
+  for (int q = threadIdx.x; q < r * b * classes; q += blockDim.x) e[q] = E[q];
+  __syncthreads();
+  if (!bias)
+    for (int q = threadIdx.x; q < r * b * kFeatF; q += blockDim.x) {
+      const int jt = q / kFeatF, f = q - jt * kFeatF;
+      xs[q] = f < nf ? __ldg(X + (int64_t)rows[jt] * in_dim + f0 + f) : 0.f;
+    }
+  __syncthreads();
+  const int nparam = bias ? classes : classes * kFeatF;
   const float fb = (float)b;
   bool bad = false;
-  for (int j = 0; j < a.r; ++j) {
-    __syncthreads();  // previous learner's tiles are consumed
-    if (threadIdx.x < b) rows[threadIdx.x] = perm[pos0 + (int64_t)(j0 + j) * b + threadIdx.x];
-    for (int q = threadIdx.x; q < b * classes; q += blockDim.x) e[q] = E[(int64_t)j * b * classes + q];
-    __syncthreads();
-    if (!bias)
-      for (int q = threadIdx.x; q < b * kFeat; q += blockDim.x) {
-        const int t = q / kFeat, f = q - t * kFeat;
-        xs[q] = f < nf ? __ldg(X + (int64_t)rows[t] * in_dim + f0 + f) : 0.f;
-      }
-    __syncthreads();
-    float* W = a.W + (int64_t)j * a.ld;
-    float* G = Gall + (int64_t)j * a.ld;
 #pragma unroll
-    for (int u = 0; u < kFusedPerThread; ++u) {
-      if (pidx[u] < 0) continue;
-      const int q = threadIdx.x + u * 256;
-      float s = 0.f;
-      if (bias) {
-        for (int t = 0; t < b; ++t) s = __fadd_rn(s, e[t * classes + q]);
-      } else {
-        const int c = q / kFeat, f = q - c * kFeat;
-        for (int t = 0; t < b; ++t) s = __fmaf_rn(e[t * classes + c], xs[t * kFeat + f], s);
+  for (int uu = 0; uu < kFusedPerThread; ++uu) {
+    const int q = threadIdx.x + uu * 256;
+    if (q >= nparam) continue;
+    const int c = bias ? q : q / kFeatF, f = bias ? 0 : q - c * kFeatF;
+    if (!bias && f >= nf) continue;
+    const int64_t p = bias ? (int64_t)classes * in_dim + c : (int64_t)c * in_dim + f0 + f;
+    const float z = a.z[p];
+    float acc = 0.f;
+    for (int j0c = 0; j0c < r; j0c += 4) {
+      float w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = (j0c + u < r) ? a.W[(int64_t)(j0c + u) * a.ld + p] : 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int j = j0c + u;
+        if (j >= r) break;
+        const float* ej = e + (int64_t)j * b * classes;
+        float s = 0.f;
+        if (bias) {
+          for (int t = 0; t < b; ++t) s = __fadd_rn(s, ej[t * classes + c]);
+        } else {
+          const float* xj = xs + (int64_t)j * b * kFeatF;
+          for (int t = 0; t < b; ++t) s = __fmaf_rn(ej[t * classes + c], xj[t * kFeatF + f], s);
+        }
+        const float g = __fdiv_rn(s, fb);
+        Gall[(int64_t)j * a.ld + p] = g;
+        const StepOut o = sma_elem(w[u], g, z, a.alpha, a.gamma);
+        a.W[(int64_t)j * a.ld + p] = o.wn;
+        acc = __fadd_rn(acc, o.c);
+        bad |= !isfinite(o.wn);
       }
-      const float g = __fdiv_rn(s, fb);
-      G[pidx[u]] = g;
-      const StepOut o = sma_elem(W[pidx[u]], g, z[u], a.alpha, a.gamma);
-      W[pidx[u]] = o.wn;
-      acc[u] = __fadd_rn(acc[u], o.c);
-      bad |= !isfinite(o.wn);
     }
-  }
-#pragma unroll
-  for (int u = 0; u < kFusedPerThread; ++u) {
-    if (pidx[u] < 0) continue;
-    const float zn = central_elem(z[u], acc[u], a.zprev_next[pidx[u]], a.mu);
-    a.zprev_next[pidx[u]] = zn;
+    const float zn = central_elem(z, acc, a.zprev_next[p], a.mu);
+    a.zprev_next[p] = zn;
     bad |= !isfinite(zn);
   }
   if (a.nonfinite && bad) atomicOr(a.nonfinite, 1);
@@ -643,16 +639,21 @@ cudaError_t launch_softmax_grad(const float* X, const int32_t* y, const int32_t*
 cudaError_t launch_softmax_round(const float* X, const int32_t* y, const int32_t* perm,
                                  int64_t pos0, int b, int in_dim, int classes, int j0, float* E,
                                  float* G, const ReplicaArgs& a, cudaStream_t s) {
-  if (classes > kMaxClasses || b > 64 || classes * kFeat > kFusedPerThread * 256)
+  if (classes > kMaxClasses || b > 64 || classes * kFeatF > kFusedPerThread * 256)
     return cudaErrorInvalidValue;
   const size_t sm1 = sizeof(float) * (size_t)in_dim;
-  const size_t sm2 = sizeof(float) * ((size_t)b * kFeat + (size_t)b * classes);
+  const size_t sm2 = sizeof(float) * ((size_t)a.r * b * kFeatF + (size_t)a.r * b * classes) +
+                     sizeof(int) * (size_t)a.r * b;
+  if (sm2 > 200 * 1024) return cudaErrorInvalidValue;
   cudaError_t e = cudaFuncSetAttribute(softmax_logits_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
   if (e != cudaSuccess) return e;
+  if ((e = cudaFuncSetAttribute(softmax_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)sm2)) != cudaSuccess)
+    return e;
   softmax_logits_kernel<<<dim3(a.r, b), classes * 32, sm1, s>>>(X, y, perm, pos0, b, in_dim, classes,
                                                                 a.W, a.ld, j0, E);
-  const int nfs = (in_dim + kFeat - 1) / kFeat;
+  const int nfs = (in_dim + kFeatF - 1) / kFeatF;
   softmax_round_kernel<<<nfs + 1, 256, sm2, s>>>(X, perm, pos0, b, in_dim, classes, j0, E, G, a);
   return cudaGetLastError();
 }

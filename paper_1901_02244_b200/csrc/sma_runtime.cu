@@ -1090,8 +1090,10 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
   if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
   if (!h->learner) return fail(SMA_ERR_STATE, "no learner attached");
   if (round < 0) return fail(SMA_ERR_INVALID_ARG, "round < 0");
+  const size_t fused_smem =
+      (sizeof(float) * (32 + (size_t)h->classes) + sizeof(int)) * (size_t)h->r * h->batch;
   const bool fusable = h->kind == 0 && !h->collective && !h->matc && h->r > 0 &&
-                       h->classes * 64 <= 3 * 256 && !h->graphs;
+                       h->classes <= 16 && fused_smem <= 200 * 1024 && !h->graphs;
   if (!fusable) {  // the same result through the two public calls
     STATUS_TRY(sma_learner_grads(h, round, stream));
     return sma_step(h, stream);
