@@ -227,12 +227,7 @@ def main():
         flags |= sma.FLAG_KERNEL_TMA
     if args.ldg:
         flags |= sma.FLAG_KERNEL_LDG
-    # libsma's default kernel policy (sma_runtime.cu): TMA on the fused path when a
-    # round streams more than 1 GiB, else the direct-load kernel
-    r_local = len(range(rank * k // world, (rank + 1) * k // world))
-    d_pad_ = sma.sma_plan_d_pad(d, world)
-    use_tma = args.tma or (not args.ldg and not collective and
-                           4.0 * d_pad_ * (3 * r_local + 3) > 1073741824.0)
+    use_tma = args.tma      # libsma's default is the direct-load kernel
     if args.matc:
         flags |= sma.FLAG_MATERIALIZE_C
     if args.zsync == "nvls" and collective:

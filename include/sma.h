@@ -91,9 +91,9 @@ enum {
     /* Replica kernel variant: TMA bulk-copy (cp.async.bulk) shared-memory
      * staging with an mbarrier pipeline (replica_step_tma) ... */
     SMA_FLAG_KERNEL_TMA = 64u,
-    /* ... or direct 128-bit loads (replica_step_ldg).  With neither flag the
-     * library picks the faster one measured on B200: TMA for the
-     * fused n = 1 round, LDG on the collective path. */
+    /* ... or direct 128-bit loads (replica_step_ldg), the default: on B200 the
+     * direct-load kernel on a full grid measured faster at every size
+     * (DESIGN.md §4). */
     SMA_FLAG_KERNEL_LDG = 128u,
     /* NEXT-1: the inter-GPU z-sync (reduce-scatter + shard update + all-gather)
      * as ONE kernel on NVSwitch multicast memory (multimem.ld_reduce /

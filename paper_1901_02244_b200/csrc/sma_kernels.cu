@@ -9,6 +9,7 @@
 // documented in DESIGN.md "Arithmetic") rather than left to FMA contraction.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "sma_internal.h"
 
@@ -99,7 +100,6 @@ __device__ __forceinline__ void replica_update4(float4& w, const float4 g, const
 // accumulation: every replica of a column is owned by the same thread, so no
 // shuffle or shared memory is needed for it.
 constexpr int kThreads = 256;
-constexpr int kUJ = 4;
 
 // Finish one float4 column chunk: the fused central update (n == 1) or the
 // per-GPU partial (collective path).
@@ -121,8 +121,8 @@ __device__ __forceinline__ void replica_finish(const ReplicaArgs& a, int64_t p0,
   }
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(kThreads, 4) replica_step_ldg(const ReplicaArgs a) {
+template <int MODE, int kUJ, int kMinBlocks = (kUJ >= 8 ? 2 : 4)>
+__global__ void __launch_bounds__(kThreads, kMinBlocks) replica_step_ldg(const ReplicaArgs a) {
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   const int64_t dfull4 = a.d >> 2;  // chunks entirely below d: vector path
   const bool matc = a.C != nullptr;
@@ -528,6 +528,56 @@ int grid_for(K kernel, int threads, size_t smem, int64_t work_items, int num_sms
   return (int)(want < 1 ? 1 : (want < cap ? want : cap));
 }
 
+// LDG launch geometry (measured, profiles/r01_ldg_variants.jsonl): one thread
+// per float4 column over a full (non-persistent) grid, replicas loaded two at a
+// time, is the fastest at every size (C4 k = 16: 6.71 TB/s vs 6.14 persistent
+// and 6.33 for the TMA ring): the hardware CTA scheduler keeps more independent
+// requests in flight than a grid-stride loop.  Knobs for experiments:
+// SMA_LDG_UNROLL = 2|4|8, SMA_LDG_GRID = full|persistent.
+int ldg_unroll() {
+  static int u = [] {
+    const char* e = getenv("SMA_LDG_UNROLL");
+    const int v = e ? atoi(e) : 2;
+    return (v == 4 || v == 8) ? v : 2;
+  }();
+  return u;
+}
+bool ldg_full_grid() {
+  static bool f = [] {
+    const char* e = getenv("SMA_LDG_GRID");
+    return !(e && e[0] == 'p');
+  }();
+  return f;
+}
+
+int ldg_minblocks() {
+  static int m = [] {
+    const char* e = getenv("SMA_LDG_MINB");
+    return e ? atoi(e) : 0;
+  }();
+  return m;
+}
+
+template <int MODE, int UJ>
+cudaError_t launch_ldg_uj(const ReplicaArgs& a, int64_t work, int num_sms, cudaStream_t s) {
+  auto k = replica_step_ldg<MODE, UJ>;
+  if (UJ == 2 && ldg_minblocks() == 6) k = replica_step_ldg<MODE, 2, 6>;
+  if (UJ == 2 && ldg_minblocks() == 8) k = replica_step_ldg<MODE, 2, 8>;
+  const int grid = ldg_full_grid() ? (int)((work + kThreads - 1) / kThreads)
+                                   : grid_for(k, kThreads, 0, work, num_sms);
+  k<<<grid < 1 ? 1 : grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int MODE>
+cudaError_t launch_ldg(const ReplicaArgs& a, int64_t work, int num_sms, cudaStream_t s) {
+  switch (ldg_unroll()) {
+    case 2: return launch_ldg_uj<MODE, 2>(a, work, num_sms, s);
+    case 8: return launch_ldg_uj<MODE, 8>(a, work, num_sms, s);
+    default: return launch_ldg_uj<MODE, 4>(a, work, num_sms, s);
+  }
+}
+
 }  // namespace
 
 // ----------------------------------------------------------------- launchers
@@ -544,29 +594,12 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
   }
   const int64_t work = a.n4 - a.c0;
   switch (mode) {
-    case kFused: {
-      auto k = replica_step_ldg<kFused>;
-      k<<<grid_for(k, kThreads, 0, work, num_sms), kThreads, 0, s>>>(a);
-      break;
-    }
-    case kPartialA: {
-      auto k = replica_step_ldg<kPartialA>;
-      k<<<grid_for(k, kThreads, 0, work, num_sms), kThreads, 0, s>>>(a);
-      break;
-    }
-    case kPartialB: {
-      auto k = replica_step_ldg<kPartialB>;
-      k<<<grid_for(k, kThreads, 0, work, num_sms), kThreads, 0, s>>>(a);
-      break;
-    }
-    case kLocal: {
-      auto k = replica_step_ldg<kLocal>;
-      k<<<grid_for(k, kThreads, 0, work, num_sms), kThreads, 0, s>>>(a);
-      break;
-    }
+    case kFused: return launch_ldg<kFused>(a, work, num_sms, s);
+    case kPartialA: return launch_ldg<kPartialA>(a, work, num_sms, s);
+    case kPartialB: return launch_ldg<kPartialB>(a, work, num_sms, s);
+    case kLocal: return launch_ldg<kLocal>(a, work, num_sms, s);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_reduce_corrections(int mode, const ReplicaArgs& a, int num_sms,

@@ -549,15 +549,9 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
   h->n4 = h->d_pad / 4;
   STATUS_TRY(sma_plan_local_replicas(cfg->k, cfg->world, cfg->rank, &h->j0, &h->r));
   STATUS_TRY(sma_plan_shard_range(cfg->d, cfg->world, cfg->rank, &h->shard_off, &h->shard_len));
-  // Default kernel policy (measured, profiles/r01_sweep_small.jsonl): the TMA
-  // pipeline wins only on the fused path once a round streams well past L2
-  // (> 1 GiB); smaller rounds are latency/occupancy-bound and the 4-CTA/SM
-  // direct-load kernel is faster.
-  {
-    const double round_bytes = 4.0 * (double)h->d_pad * (3.0 * h->r + 3.0);
-    h->tma = (f & SMA_FLAG_KERNEL_TMA) ||
-             (!(f & SMA_FLAG_KERNEL_LDG) && !h->collective && round_bytes > 1073741824.0);
-  }
+  // Kernel policy: the direct-load kernel on a full grid is the fastest at every
+  // measured size (profiles/r01_ldg_variants.jsonl); the TMA ring on request.
+  h->tma = (f & SMA_FLAG_KERNEL_TMA) != 0;
   if (h->r > SMA_MAX_LOCAL_REPLICAS)
     return fail(SMA_ERR_INVALID_ARG, "%d replicas on rank %d exceeds SMA_MAX_LOCAL_REPLICAS=%d",
                 h->r, cfg->rank, SMA_MAX_LOCAL_REPLICAS);
