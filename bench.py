@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--force-collective", action="store_true")
     ap.add_argument("--zsync", choices=["nccl", "nvls"], default="nccl",
                     help="inter-GPU z-sync: NCCL RS/AG (default) or the fused multicast kernel")
+    ap.add_argument("--tau", type=int, default=1,
+                    help="synchronise every tau iterations (sma_step_local on the others; "
+                         "0 = never: the paper's 'no synchronisation' point, fig:overhead)")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -260,7 +263,13 @@ def main():
         h.synth_grads(0, sma_inputs.SEED_G, stream)   # inputs resident in HBM before timing
 
         def one_step():
-            h.step(stream)
+            # tau = 1: every iteration is a full SMA round; tau > 1 / 0: the E11
+            # analog with local-only iterations in between
+            rnd[0] += 1
+            if args.tau == 1 or (args.tau > 1 and rnd[0] % args.tau == 0):
+                h.step(stream)
+            else:
+                h.step_local(stream)
     stream.synchronize()
 
     def barrier():
@@ -350,6 +359,10 @@ def main():
             kname = f"replica_step_{kvar}<kPartial{mode}>"
         if args.matc:
             alg_bytes = 4 * d_pad * (6 * r + (3 if mode == "fused" else 2))
+        if args.tau != 1 and not learner:   # mix of sync rounds and local-only iterations
+            n_sync = (args.steps // args.tau) if args.tau > 1 else 0
+            alg_bytes = (n_sync * alg_bytes + (args.steps - n_sync) * 4 * d_pad * 3 * r) / args.steps
+            kname += " / replica_step_ldg<kLocal>"
         achieved = alg_bytes / (kern_avg * 1e-3) / 1e9
         traffic = None
         tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_n{world}_{mode}_{kvar}.json")
@@ -400,6 +413,10 @@ def main():
                                    if mode == "B" else "")}
         if e2e:
             line["e2e"] = e2e
+        if args.tau != 1:
+            line["config"]["tau"] = args.tau
+            line["config"]["note"] = ("E11 analog (P:1476-1503): iterations/s with "
+                                      "synchronisation every tau iterations (0 = never)")
         if learner:
             line["config"]["learner"] = args.config
             line["config"]["batch"] = cfg["batch"]

@@ -570,7 +570,13 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
                 prop.major, prop.minor);
   h->num_sms = prop.multiProcessorCount;
 
-  CUDA_TRY(cudaStreamCreateWithFlags(&h->sB, cudaStreamNonBlocking));
+  {  // the z-sync stream gets the highest priority, so in Mode B the CTA
+     // scheduler dispatches NCCL's / the shard update's CTAs ahead of the
+     // (full-grid) replica kernel's remaining CTAs instead of after them
+    int least = 0, greatest = 0;
+    CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CUDA_TRY(cudaStreamCreateWithPriority(&h->sB, cudaStreamNonBlocking, greatest));
+  }
   CUDA_TRY(cudaStreamCreateWithFlags(&h->sIO, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&h->evFork, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&h->evJoin, cudaEventDisableTiming));
@@ -801,7 +807,11 @@ sma_status sma_step_local(sma_handle* h, void* stream) {
   a.n4 = h->n4;
   a.gamma = h->gamma;
   a.nonfinite = h->check ? h->nonfinite : nullptr;
+  cudaEvent_t* tp = nullptr;
+  STATUS_TRY(timer_pair(h, SMA_PHASE_REPLICA, &tp));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
   CUDA_TRY(launch_replica_step(kLocal, false, a, h->num_sms, s));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
   ++h->launches;
   h->q_dirty = true;  // Mode B: Q^i = sum_j (w_j - z_prev) must be recomputed
   return mark_done(h, s);
