@@ -546,3 +546,32 @@ def test_learner_step_fused_is_bitwise_unfused(torch_cuda, S, orc):
     assert relerr(hs[0].central(), zr) <= TOL
     for h in hs:
         h.close()
+
+
+def test_randomized_configs(torch_cuda, S, orc):
+    """30 random configurations (d, k, alpha, gamma, mu, variant), 20 rounds each,
+    vs the oracle: catches size/alignment/replica-count corner cases (d % 4,
+    r not a multiple of the load batch, tiny d, r = 1)."""
+    rng = np.random.default_rng(2024)
+    variants = [0, 2, 8, 64, 128, 16, 16 | 1, 16 | 2, 16 | 1 | 8, 16 | 64]
+    s = torch_cuda.cuda.Stream()
+    for trial in range(30):
+        d = int(rng.choice([1, 2, 3, 5, 63, 64, 65, 511, 513, 2047, 2049, 4099, 12345,
+                            int(rng.integers(1, 300_000))]))
+        k = int(rng.integers(1, 21))
+        a = F32(rng.uniform(0.0, 1.0 / k))
+        g = F32(rng.uniform(0.0, 0.2))
+        m = F32(rng.uniform(0.0, 0.95))
+        flags = int(rng.choice(variants))
+        R = 20
+        h = S.Sma(d, k, a, g, m, sma_inputs.w0(d), flags=flags)
+        for i in range(R):
+            h.synth_grads(i, sma_inputs.SEED_G, s)
+            h.step(s)
+        zr, zpr, Wr = orc.run_synth(d, k, a, g, m, R, sma_inputs.SEED_W, sma_inputs.SEED_G)
+        ctx = dict(trial=trial, d=d, k=k, a=a, g=g, m=m, flags=flags)
+        assert relerr(h.central(), zr) <= TOL, ctx
+        assert relerr(h.central_prev(), zpr) <= TOL, ctx
+        for j in range(k):
+            assert relerr(h.replica(j), Wr[j]) <= TOL, ctx
+        h.close()
