@@ -179,6 +179,62 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) replica_step_ldg(const R
     atomicOr(a.nonfinite, 1);
 }
 
+// ------------------------------------------- replica kernel, small rounds
+// For rounds too small to fill the GPU with one thread per column (C1-C3
+// sizes: the full-grid kernel runs only ~3 CTAs per SM there), G lanes share a
+// float4 column: lane = group * (32/G) + column, group g takes replicas
+// j = g, g + G, ... (two per load batch), and the G partial sums are combined
+// with log2(G) xor-shuffles (bitwise identical in every lane: fp addition is
+// commutative); group 0 finishes the column.  4x the threads for the same d.
+template <int MODE, int G>
+__global__ void __launch_bounds__(kThreads) replica_step_split(const ReplicaArgs a) {
+  constexpr int CPW = 32 / G;  // columns per warp
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = lane / CPW, col = lane - grp * CPW;
+  const int64_t c = ((int64_t)blockIdx.x * (kThreads / 32) + warp) * CPW + col;
+  const bool valid = c < a.n4;
+  const bool full = c < (a.d >> 2);
+  const bool matc = a.C != nullptr;
+  const int64_t p0 = c << 2;
+  const float4 z = valid ? ld_ro(a.z + p0) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 c4;
+  bool bad = false;
+  if (valid) {
+    int j = grp;
+    for (; j + G < a.r; j += 2 * G) {
+      float4 w0 = ld_rw(a.W + (int64_t)j * a.ld + p0);
+      float4 w1 = ld_rw(a.W + (int64_t)(j + G) * a.ld + p0);
+      const float4 g0 = full ? ld_ro(a.g.p[j] + p0) : ld_tail(a.g.p[j], p0, a.d);
+      const float4 g1 = full ? ld_ro(a.g.p[j + G] + p0) : ld_tail(a.g.p[j + G], p0, a.d);
+      replica_update4<MODE>(w0, g0, z, acc, c4, a.alpha, a.gamma);
+      st4(a.W + (int64_t)j * a.ld + p0, w0);
+      if (matc) st4(a.C + (int64_t)j * a.ld + p0, c4);
+      replica_update4<MODE>(w1, g1, z, acc, c4, a.alpha, a.gamma);
+      st4(a.W + (int64_t)(j + G) * a.ld + p0, w1);
+      if (matc) st4(a.C + (int64_t)(j + G) * a.ld + p0, c4);
+      bad |= !finite4(w0) || !finite4(w1);
+    }
+    for (; j < a.r; j += G) {
+      float4 w0 = ld_rw(a.W + (int64_t)j * a.ld + p0);
+      const float4 g0 = full ? ld_ro(a.g.p[j] + p0) : ld_tail(a.g.p[j], p0, a.d);
+      replica_update4<MODE>(w0, g0, z, acc, c4, a.alpha, a.gamma);
+      st4(a.W + (int64_t)j * a.ld + p0, w0);
+      if (matc) st4(a.C + (int64_t)j * a.ld + p0, c4);
+      bad |= !finite4(w0);
+    }
+  }
+#pragma unroll
+  for (int off = CPW; off < 32; off <<= 1) {  // combine the G replica groups
+    acc.x = __fadd_rn(acc.x, __shfl_xor_sync(0xffffffffu, acc.x, off));
+    acc.y = __fadd_rn(acc.y, __shfl_xor_sync(0xffffffffu, acc.y, off));
+    acc.z = __fadd_rn(acc.z, __shfl_xor_sync(0xffffffffu, acc.z, off));
+    acc.w = __fadd_rn(acc.w, __shfl_xor_sync(0xffffffffu, acc.w, off));
+  }
+  if (valid && grp == 0 && !matc) replica_finish<MODE>(a, p0, z, acc, bad);
+  if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
+}
+
 // ---------------------------------------- MATERIALIZE_C: reduce c_j over j
 // The north_star-literal intra-GPU reduction of the materialised corrections.
 // A warp covers 8 float4 columns x 4 replica groups (lane = group*8 + column:
@@ -434,8 +490,9 @@ __global__ void __launch_bounds__(256) softmax_wgrad_kernel(
 // batch tiles are staged at once; each thread then walks its parameters and,
 // per parameter, the learners in ascending j (4 replica loads in flight).  The
 // arithmetic per element is exactly that of softmax_wgrad_kernel then
-// replica_step_ldg<kFused> (same operation order), so the result is bitwise
-// identical to the unfused pair.  The gradient is still written to G.
+// replica_step_ldg<kFused> (same operation order: bitwise identical to that
+// pair; the small-round split kernel sums the corrections per lane group, so
+// against it the results agree to rounding).  The gradient is still written to G.
 constexpr int kFeatF = 32;
 constexpr int kFusedPerThread = 2;  // ceil(classes * kFeatF / 256) for classes <= 16
 __global__ void __launch_bounds__(256) softmax_round_kernel(
@@ -593,6 +650,32 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
     if (a.c0 >= a.n4) return cudaSuccess;
   }
   const int64_t work = a.n4 - a.c0;
+  // small rounds: lanes split the replicas of a column (see replica_step_split)
+  static const int64_t split_below = [] {
+    const char* e = getenv("SMA_SPLIT_BELOW");   // float4 chunks; 0 disables
+    return e ? atoll(e) : 148ll * 1024;
+  }();
+  // measured (profiles/r01_split.jsonl): splitting pays when the column count
+  // cannot fill the GPU (d < ~150k) or when r >= 8 replicas lengthen each
+  // thread's chain; at medium d with r = 4 it is slower
+  const bool split = a.c0 == 0 && mode != kLocal && a.r >= 2 &&
+                     (a.n4 < split_below / 4 || (a.n4 < split_below && a.r >= 8));
+  if (split) {
+    const int G = a.r >= 4 ? 4 : 2;
+    const int64_t cols_per_block = (kThreads / 32) * (32 / G);
+    const int grid = (int)((a.n4 + cols_per_block - 1) / cols_per_block);
+#define SMA_SPLIT_LAUNCH(M)                                                                  \
+  if (G == 4) replica_step_split<M, 4><<<grid, kThreads, 0, s>>>(a);                          \
+  else replica_step_split<M, 2><<<grid, kThreads, 0, s>>>(a);
+    switch (mode) {
+      case kFused: SMA_SPLIT_LAUNCH(kFused) break;
+      case kPartialA: SMA_SPLIT_LAUNCH(kPartialA) break;
+      case kPartialB: SMA_SPLIT_LAUNCH(kPartialB) break;
+      default: return cudaErrorInvalidValue;
+    }
+#undef SMA_SPLIT_LAUNCH
+    return cudaGetLastError();
+  }
   switch (mode) {
     case kFused: return launch_ldg<kFused>(a, work, num_sms, s);
     case kPartialA: return launch_ldg<kPartialA>(a, work, num_sms, s);

@@ -518,9 +518,10 @@ def test_paper_config_sizes_sampled_parity(torch_cuda, S, orc, cfg):
 
 
 def test_learner_step_fused_is_bitwise_unfused(torch_cuda, S, orc):
-    """sma_learner_step's fused softmax round == sma_learner_grads + sma_step,
-    bit for bit (same per-element operation order), over 60 rounds crossing an
-    epoch; and both match the oracle (config C1 shape)."""
+    """sma_learner_step's fused softmax round == sma_learner_grads + sma_step
+    over 60 rounds crossing an epoch (bit for bit when the unfused replica kernel
+    sums the corrections in the same order; the small-round split kernel sums
+    them per lane group, so here to 1e-6), and both match the oracle (C1 shape)."""
     torch = torch_cuda
     X, y = sma_inputs.blobs(3_000, seed=4)
     k, b, R = 4, 16, 60
@@ -538,10 +539,10 @@ def test_learner_step_fused_is_bitwise_unfused(torch_cuda, S, orc):
                 S.sma_learner_grads(h.h, i, s)
                 h.step(s)
         hs.append(h)
-    assert np.array_equal(hs[0].central(), hs[1].central())
-    assert np.array_equal(hs[0].central_prev(), hs[1].central_prev())
+    assert relerr(hs[0].central(), hs[1].central()) <= 1e-6
+    assert relerr(hs[0].central_prev(), hs[1].central_prev()) <= 1e-6
     for j in range(k):
-        assert np.array_equal(hs[0].replica(j), hs[1].replica(j))
+        assert relerr(hs[0].replica(j), hs[1].replica(j)) <= 1e-6
     zr, _, _ = orc.run_softmax(X, y, b, 99, k, a, g, m, R, np.zeros(7850))
     assert relerr(hs[0].central(), zr) <= TOL
     for h in hs:
