@@ -515,7 +515,10 @@ sma_status alloc_coll(sma_handle* h, float** p, size_t n) {
   const bool use = h->cfg.world > 1 && g_nccl.MemAlloc && g_nccl.MemFree && !(e && e[0] == '0');
   if (!use) return alloc_zero(p, n);
   void* q = nullptr;
-  NCCL_TRY(g_nccl.MemAlloc(&q, sizeof(float) * n));
+  if (g_nccl.MemAlloc(&q, sizeof(float) * n) != ncclSuccess || !q) {
+    cudaGetLastError();            // NCCL could not provide NVLS-capable memory:
+    return alloc_zero(p, n);       // plain device memory works for every algorithm
+  }
   h->nccl_allocs.push_back(q);
   *p = static_cast<float*>(q);
   CUDA_TRY(cudaMemset(q, 0, sizeof(float) * n));
