@@ -11,6 +11,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include "sma_bulk.cuh"
 #include "sma_internal.h"
 
 namespace sma {
@@ -403,17 +404,14 @@ __global__ void __launch_bounds__(kMaxClasses * 32) softmax_logits_kernel(
   extern __shared__ __align__(16) float xs[];  // [in_dim]
   __shared__ float lg[kMaxClasses];
   const int slot = blockIdx.x, t = blockIdx.y;
-  const int row = perm[pos0 + (int64_t)(j0 + slot) * b + t];
-  const float* x = X + (int64_t)row * in_dim;
+  __shared__ int row_sm;
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) row_sm = perm[pos0 + (int64_t)(j0 + slot) * b + t];
+  __syncthreads();
+  const int row = row_sm;
   const float* W = Wall + (int64_t)slot * ld;
   const bool vec = (in_dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
-  if (vec) {
-    for (int q = threadIdx.x; q < (in_dim >> 2); q += blockDim.x)
-      reinterpret_cast<float4*>(xs)[q] = __ldg(reinterpret_cast<const float4*>(x) + q);
-  } else {
-    for (int q = threadIdx.x; q < in_dim; q += blockDim.x) xs[q] = x[q];
-  }
-  __syncthreads();
+  bulk::stage_rows_span(xs, X, &row_sm, 1, in_dim, in_dim, 0, nullptr, nullptr, 0, &bar, 0, true);
   const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
   if (c < classes) {  // warp c: logit of class c, W row c read straight from L2
     const float* w = W + (int64_t)c * in_dim;
@@ -459,20 +457,17 @@ __global__ void __launch_bounds__(256) softmax_wgrad_kernel(
   const int slot = blockIdx.x, f0 = blockIdx.y * kFeat;
   const int nf = min(kFeat, in_dim - f0);
   float* G = Gall + (int64_t)slot * ld;
+  __shared__ __align__(8) uint64_t bar;
   if (threadIdx.x < b) rows[threadIdx.x] = perm[pos0 + (int64_t)(j0 + slot) * b + threadIdx.x];
   for (int q = threadIdx.x; q < b * classes; q += blockDim.x) e[q] = E[(int64_t)slot * b * classes + q];
   __syncthreads();
-  for (int q = threadIdx.x; q < b * kFeat; q += blockDim.x) {
-    const int t = q / kFeat, f = q - t * kFeat;
-    xs[q] = f < nf ? __ldg(X + (int64_t)rows[t] * in_dim + f0 + f) : 0.f;
-  }
-  __syncthreads();
+  // X[rows][f0, f0 + nf) -> xs [b][nf] in one TMA bulk transaction
+  bulk::stage_rows_span(xs, X, rows, b, nf, in_dim, f0, nullptr, nullptr, 0, &bar, 0, true);
   const float fb = (float)b;
-  for (int q = threadIdx.x; q < classes * kFeat; q += blockDim.x) {
-    const int c = q / kFeat, f = q - c * kFeat;
-    if (f >= nf) continue;
+  for (int q = threadIdx.x; q < classes * nf; q += blockDim.x) {
+    const int c = q / nf, f = q - c * nf;
     float s = 0.f;
-    for (int t = 0; t < b; ++t) s = __fmaf_rn(e[t * classes + c], xs[t * kFeat + f], s);
+    for (int t = 0; t < b; ++t) s = __fmaf_rn(e[t * classes + c], xs[t * nf + f], s);
     G[(int64_t)c * in_dim + f0 + f] = __fdiv_rn(s, fb);
   }
   if (blockIdx.y == 0 && threadIdx.x < classes) {
@@ -512,13 +507,10 @@ __global__ void __launch_bounds__(256) softmax_round_kernel(
     rows[q] = perm[pos0 + (int64_t)(j0 + j) * b + t];
   }
   for (int q = threadIdx.x; q < r * b * classes; q += blockDim.x) e[q] = E[q];
+  __shared__ __align__(8) uint64_t bar;
   __syncthreads();
-  if (!bias)
-    for (int q = threadIdx.x; q < r * b * kFeatF; q += blockDim.x) {
-      const int jt = q / kFeatF, f = q - jt * kFeatF;
-      xs[q] = f < nf ? __ldg(X + (int64_t)rows[jt] * in_dim + f0 + f) : 0.f;
-    }
-  __syncthreads();
+  // every learner's X[rows][f0, f0 + nf) -> xs [r*b][nf] in one TMA bulk transaction
+  if (!bias) bulk::stage_rows_span(xs, X, rows, r * b, nf, in_dim, f0, nullptr, nullptr, 0, &bar, 0, true);
   const int nparam = bias ? classes : classes * kFeatF;
   const float fb = (float)b;
   bool bad = false;
@@ -544,8 +536,8 @@ __global__ void __launch_bounds__(256) softmax_round_kernel(
         if (bias) {
           for (int t = 0; t < b; ++t) s = __fadd_rn(s, ej[t * classes + c]);
         } else {
-          const float* xj = xs + (int64_t)j * b * kFeatF;
-          for (int t = 0; t < b; ++t) s = __fmaf_rn(ej[t * classes + c], xj[t * kFeatF + f], s);
+          const float* xj = xs + (int64_t)j * b * nf;
+          for (int t = 0; t < b; ++t) s = __fmaf_rn(ej[t * classes + c], xj[t * nf + f], s);
         }
         const float g = __fdiv_rn(s, fb);
         Gall[(int64_t)j * a.ld + p] = g;

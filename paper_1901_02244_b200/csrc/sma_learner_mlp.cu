@@ -4,8 +4,9 @@
 //
 // Three small kernels per round (the learner is latency-bound at b = 16):
 //   1. mlp_hidden_kernel  grid (r, hidden/8): gather the batch rows into shared
-//      memory; pre-activations a1 = W1 x + b1 accumulated in double-float
-//      (Dot2, ~2^-48; R18: the ReLU mask is an integer decision, taken at
+//      memory; pre-activations a1 = W1 x + b1 in fp32 with an a-priori error
+//      bound, recomputed in double-float (Dot2, ~2^-48) when the fp32 sign is
+//      not certain (R18: the ReLU mask is an integer decision, taken at
 //      fp64-level accuracy on both sides, so the GPU and the fp64 oracle agree
 //      on it except within ~1e-13 of a kink).
 //   2. mlp_head_kernel    grid (r): h = relu(a1) (fp32), logits, max-subtracted
@@ -15,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "sma_bulk.cuh"
 #include "sma_internal.h"
 
 namespace sma {
@@ -26,33 +28,6 @@ constexpr int kHeadSplit = 8;    // CTAs per learner of the head kernel
 
 __device__ __forceinline__ int batch_row(const int32_t* perm, int64_t pos0, int j, int b, int t) {
   return perm[pos0 + (int64_t)j * b + t];
-}
-
-// Stage the b batch rows of X into xs[t][in_dim] (128-bit loads when aligned).
-__device__ __forceinline__ void stage_batch(float* xs, const float* __restrict__ X,
-                                            const int32_t* __restrict__ perm, int64_t pos0, int j,
-                                            int b, int in_dim) {
-  if ((in_dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(X) & 15) == 0)) {
-    const int v = in_dim >> 2;
-    for (int q = threadIdx.x; q < b * v; q += blockDim.x) {
-      const int t = q / v, f4 = q - t * v;
-      reinterpret_cast<float4*>(xs)[q] = __ldg(
-          reinterpret_cast<const float4*>(X + (int64_t)batch_row(perm, pos0, j, b, t) * in_dim) + f4);
-    }
-  } else {
-    for (int q = threadIdx.x; q < b * in_dim; q += blockDim.x) {
-      const int t = q / in_dim, f = q - t * in_dim;
-      xs[q] = X[(int64_t)batch_row(perm, pos0, j, b, t) * in_dim + f];
-    }
-  }
-}
-__device__ __forceinline__ void stage_span(float* dst, const float* __restrict__ src, int n) {
-  if ((n & 3) == 0 && ((reinterpret_cast<uintptr_t>(src) & 15) == 0)) {
-    for (int q = threadIdx.x; q < (n >> 2); q += blockDim.x)
-      reinterpret_cast<float4*>(dst)[q] = __ldg(reinterpret_cast<const float4*>(src) + q);
-  } else {
-    for (int q = threadIdx.x; q < n; q += blockDim.x) dst[q] = src[q];
-  }
 }
 
 // Error-free transformations (Knuth TwoSum, FMA TwoProd): the Ogita-Rump-Oishi
@@ -93,39 +68,60 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_hidden_kernel(
   const int nu = min(kHidUnits, hidden - k0);
   const float* W1 = Wall + (int64_t)slot * ld;
   const float* b1 = W1 + (int64_t)hidden * in_dim;
-  stage_batch(xs, X, perm, pos0, j0 + slot, b, in_dim);
-  stage_span(ws, W1 + (int64_t)k0 * in_dim, nu * in_dim);
+  __shared__ int rows[64];
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x < b) rows[threadIdx.x] = batch_row(perm, pos0, j0 + slot, b, threadIdx.x);
   __syncthreads();
+  // the batch rows and this CTA's W1 rows in one TMA bulk transaction
+  bulk::stage_rows_span(xs, X, rows, b, in_dim, in_dim, 0, ws, W1 + (int64_t)k0 * in_dim,
+                        nu * in_dim, &bar, 0, true);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int pr = warp; pr < b * nu; pr += nw) {
     const int t = pr / nu, u = pr - t * nu;
     const float* w = ws + (int64_t)u * in_dim;
     const float* x = xs + (int64_t)t * in_dim;
-    f2 acc = {0.f, 0.f};
-    if ((in_dim & 3) == 0) {
-      const float4* w4 = reinterpret_cast<const float4*>(w);
-      const float4* x4 = reinterpret_cast<const float4*>(x);
-      for (int f = lane; f < (in_dim >> 2); f += 32) {
-        const float4 a = w4[f], c = x4[f];
-        dot2_step(acc, a.x, c.x);
-        dot2_step(acc, a.y, c.y);
-        dot2_step(acc, a.z, c.z);
-        dot2_step(acc, a.w, c.w);
-      }
-    } else {
-      for (int f = lane; f < in_dim; f += 32) dot2_step(acc, w[f], x[f]);
+    // fast path: plain fp32 dot and sum_f |w x|; the fp32 result's sign is
+    // certain unless |a| <= 2^-12 sum|w x| (> 3x the n u sum|w x| error bound
+    // for n <= 1024), and only then (rare; warp-uniform) is the dot redone
+    // with the Dot2 accumulation.
+    float sv = 0.f, sa = 0.f;
+    for (int f = lane; f < in_dim; f += 32) {
+      sv = __fmaf_rn(w[f], x[f], sv);
+      sa = __fmaf_rn(fabsf(w[f]), fabsf(x[f]), sa);
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
-      f2 o;
-      o.hi = __shfl_xor_sync(0xffffffffu, acc.hi, off);
-      o.lo = __shfl_xor_sync(0xffffffffu, acc.lo, off);
-      acc = f2_add(acc, o);
+      sv = __fadd_rn(sv, __shfl_xor_sync(0xffffffffu, sv, off));
+      sa = __fadd_rn(sa, __shfl_xor_sync(0xffffffffu, sa, off));
     }
-    if (lane == 0) {
-      acc = f2_add(acc, f2{b1[k0 + u], 0.f});
-      A1[((int64_t)slot * b + t) * hidden + k0 + u] = make_float2(acc.hi, acc.lo);
+    const float bias = b1[k0 + u];
+    f2 acc = {__fadd_rn(sv, bias), 0.f};
+    const float bound = ldexpf(__fadd_rn(sa, fabsf(bias)), -12);
+    if (fabsf(acc.hi) <= bound) {  // near a ReLU kink: decide at ~2^-48
+      acc = f2{0.f, 0.f};
+      if ((in_dim & 3) == 0) {
+        const float4* w4 = reinterpret_cast<const float4*>(w);
+        const float4* x4 = reinterpret_cast<const float4*>(x);
+        for (int f = lane; f < (in_dim >> 2); f += 32) {
+          const float4 a = w4[f], c = x4[f];
+          dot2_step(acc, a.x, c.x);
+          dot2_step(acc, a.y, c.y);
+          dot2_step(acc, a.z, c.z);
+          dot2_step(acc, a.w, c.w);
+        }
+      } else {
+        for (int f = lane; f < in_dim; f += 32) dot2_step(acc, w[f], x[f]);
+      }
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        f2 o;
+        o.hi = __shfl_xor_sync(0xffffffffu, acc.hi, off);
+        o.lo = __shfl_xor_sync(0xffffffffu, acc.lo, off);
+        acc = f2_add(acc, o);
+      }
+      acc = f2_add(acc, f2{bias, 0.f});
     }
+    if (lane == 0) A1[((int64_t)slot * b + t) * hidden + k0 + u] = make_float2(acc.hi, acc.lo);
   }
 }
 
@@ -143,13 +139,19 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_head_kernel(
   float* G = Gall + (int64_t)slot * ld;
   float* gW2 = G + (int64_t)hidden * in_dim + hidden;
   float* gb2 = gW2 + (int64_t)classes * hidden;
-  const float2* a1 = A1 + (int64_t)slot * b * hidden;
+  float2* a1 = reinterpret_cast<float2*>(e + ((b * classes + 3) & ~3));  // staged copy of A1
+  __shared__ int zero_row;
+  __shared__ __align__(8) uint64_t bar;
+  if (threadIdx.x == 0) zero_row = 0;
+  __syncthreads();
+  bulk::stage_rows_span(reinterpret_cast<float*>(a1),
+                        reinterpret_cast<const float*>(A1 + (int64_t)slot * b * hidden), &zero_row,
+                        1, 2 * b * hidden, 0, 0, w2s, W2, classes * hidden, &bar, 0, true);
   // relu on the double-float pre-activation: positive iff hi > 0, or hi == 0 and lo > 0
   for (int q = threadIdx.x; q < b * hidden; q += blockDim.x) {
     const float2 v = a1[q];
     hs[q] = (v.x > 0.f || (v.x == 0.f && v.y > 0.f)) ? __fadd_rn(v.x, v.y) : 0.f;
   }
-  stage_span(w2s, W2, classes * hidden);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int pr = warp; pr < b * classes; pr += nw) {  // logits
@@ -211,28 +213,27 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_w1_kernel(
   const int slot = blockIdx.x, k0 = blockIdx.y * kUnits, f0 = blockIdx.z * kFeat;
   const int nf = min(kFeat, in_dim - f0);
   float* G = Gall + (int64_t)slot * ld;
+  __shared__ __align__(8) uint64_t bar;
+  const int nu = min(kUnits, hidden - k0);
   if (threadIdx.x < b) rows[threadIdx.x] = batch_row(perm, pos0, j0 + slot, b, threadIdx.x);
-  for (int q = threadIdx.x; q < b * kUnits; q += blockDim.x) {
-    const int t = q / kUnits, u = q - t * kUnits;
-    da[q] = (k0 + u < hidden) ? DA[((int64_t)slot * b + t) * hidden + k0 + u] : 0.f;
-  }
   __syncthreads();
-  for (int q = threadIdx.x; q < b * kFeat; q += blockDim.x) {
-    const int t = q / kFeat, f = q - t * kFeat;
-    xs[q] = f < nf ? __ldg(X + (int64_t)rows[t] * in_dim + f0 + f) : 0.f;
+  // da1[t][k0, k0 + nu) -> da [b][nu] with plain loads (in flight while) the
+  // X[rows][f0, f0 + nf) -> xs [b][nf] TMA bulk transaction completes
+  for (int q = threadIdx.x; q < b * nu; q += blockDim.x) {
+    const int t = q / nu, u = q - t * nu;
+    da[q] = DA[((int64_t)slot * b + t) * hidden + k0 + u];
   }
-  __syncthreads();
+  bulk::stage_rows_span(xs, X, rows, b, nf, in_dim, f0, nullptr, nullptr, 0, &bar, 0, true);
   const float fb = (float)b;
-  for (int q = threadIdx.x; q < kUnits * kFeat; q += blockDim.x) {  // dW1 = da^T x / b
-    const int u = q / kFeat, f = q - u * kFeat;
-    if (k0 + u >= hidden || f >= nf) continue;
+  for (int q = threadIdx.x; q < nu * nf; q += blockDim.x) {  // dW1 = da^T x / b
+    const int u = q / nf, f = q - u * nf;
     float s = 0.f;
-    for (int t = 0; t < b; ++t) s = __fmaf_rn(da[t * kUnits + u], xs[t * kFeat + f], s);
+    for (int t = 0; t < b; ++t) s = __fmaf_rn(da[t * nu + u], xs[t * nf + f], s);
     G[(int64_t)(k0 + u) * in_dim + f0 + f] = __fdiv_rn(s, fb);
   }
-  if (blockIdx.z == 0 && threadIdx.x < kUnits && k0 + threadIdx.x < hidden) {
+  if (blockIdx.z == 0 && threadIdx.x < nu) {
     float s = 0.f;
-    for (int t = 0; t < b; ++t) s = __fadd_rn(s, da[t * kUnits + threadIdx.x]);
+    for (int t = 0; t < b; ++t) s = __fadd_rn(s, da[t * nu + threadIdx.x]);
     G[(int64_t)hidden * in_dim + k0 + threadIdx.x] = __fdiv_rn(s, fb);
   }
 }
@@ -243,7 +244,8 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
                             int r, int j0, float2* A1, float* DA, float* G, cudaStream_t s) {
   const size_t sm1 = sizeof(float) * ((size_t)b * in_dim + (size_t)kHidUnits * in_dim);
   const size_t sm2 = sizeof(float) * ((size_t)b * hidden + (size_t)classes * hidden +
-                                      (size_t)b * classes);
+                                      (size_t)b * classes) +
+                     16 + sizeof(float2) * (size_t)b * hidden;
   const size_t sm3 = sizeof(float) * ((size_t)b * kFeat + (size_t)b * kUnits);
   cudaError_t e;
   if ((e = cudaFuncSetAttribute(mlp_hidden_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
