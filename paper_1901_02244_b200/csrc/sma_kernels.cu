@@ -37,6 +37,47 @@ __device__ __forceinline__ void st4(float* p, float4 v) {
   asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};"
                :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
+// Cache-policy variants of the streaming ops (experiment knob SMA_LDG_POLICY,
+// profiles/r01_ldg_policy.jsonl): 1 = evict-first streaming (.cs) loads and
+// stores of the replica/gradient streams, 2 = 256-byte L2 prefetch on loads.
+template <int POL>
+__device__ __forceinline__ float4 ld_rw_p(const float* p) {
+  float4 v;
+  if (POL == 1)
+    asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  else if (POL == 2)
+    asm volatile("ld.global.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  else
+    asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+template <int POL>
+__device__ __forceinline__ float4 ld_ro_p(const float* p) {
+  float4 v;
+  if (POL == 1)
+    asm volatile("ld.global.cs.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  else if (POL == 2)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  else
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+  return v;
+}
+template <int POL>
+__device__ __forceinline__ void st4_p(float* p, float4 v) {
+  if (POL == 1)
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+  else
+    asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};"
+                 :: "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+
 // Gradient chunk that straddles (or lies beyond) d: scalar loads, zeros past d.
 __device__ __forceinline__ float4 ld_tail(const float* g, int64_t p0, int64_t d) {
   float4 v;
@@ -122,7 +163,7 @@ __device__ __forceinline__ void replica_finish(const ReplicaArgs& a, int64_t p0,
   }
 }
 
-template <int MODE, int kUJ, int kMinBlocks = (kUJ >= 8 ? 2 : 4)>
+template <int MODE, int kUJ, int kMinBlocks = (kUJ >= 8 ? 2 : 4), int POL = 0>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) replica_step_ldg(const ReplicaArgs a) {
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   const int64_t dfull4 = a.d >> 2;  // chunks entirely below d: vector path
@@ -137,13 +178,13 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) replica_step_ldg(const R
     for (; j + kUJ <= a.r; j += kUJ) {
       float4 w[kUJ], g[kUJ];
 #pragma unroll
-      for (int u = 0; u < kUJ; ++u) w[u] = ld_rw(a.W + (int64_t)(j + u) * a.ld + p0);
+      for (int u = 0; u < kUJ; ++u) w[u] = ld_rw_p<POL>(a.W + (int64_t)(j + u) * a.ld + p0);
 #pragma unroll
-      for (int u = 0; u < kUJ; ++u) g[u] = ld_ro(a.g.p[j + u] + p0);
+      for (int u = 0; u < kUJ; ++u) g[u] = ld_ro_p<POL>(a.g.p[j + u] + p0);
 #pragma unroll
       for (int u = 0; u < kUJ; ++u) {
         replica_update4<MODE>(w[u], g[u], z, acc, c4, a.alpha, a.gamma);
-        st4(a.W + (int64_t)(j + u) * a.ld + p0, w[u]);
+        st4_p<POL>(a.W + (int64_t)(j + u) * a.ld + p0, w[u]);
         if (matc) st4(a.C + (int64_t)(j + u) * a.ld + p0, c4);
         bad |= !finite4(w[u]);
       }
@@ -607,9 +648,19 @@ int ldg_minblocks() {
   return m;
 }
 
+int ldg_policy() {
+  static int p = [] {
+    const char* e = getenv("SMA_LDG_POLICY");
+    return e ? atoi(e) : 0;
+  }();
+  return p;
+}
+
 template <int MODE, int UJ>
 cudaError_t launch_ldg_uj(const ReplicaArgs& a, int64_t work, int num_sms, cudaStream_t s) {
   auto k = replica_step_ldg<MODE, UJ>;
+  if (UJ == 2 && ldg_policy() == 1) k = replica_step_ldg<MODE, 2, 4, 1>;
+  if (UJ == 2 && ldg_policy() == 2) k = replica_step_ldg<MODE, 2, 4, 2>;
   if (UJ == 2 && ldg_minblocks() == 6) k = replica_step_ldg<MODE, 2, 6>;
   if (UJ == 2 && ldg_minblocks() == 8) k = replica_step_ldg<MODE, 2, 8>;
   const int grid = ldg_full_grid() ? (int)((work + kThreads - 1) / kThreads)

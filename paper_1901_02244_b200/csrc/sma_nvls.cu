@@ -25,6 +25,7 @@
 #include <sys/un.h>
 #include <unistd.h>
 
+#include <mutex>
 #include <string>
 
 #include "sma_internal.h"
@@ -73,11 +74,15 @@ bool bind_sym(F*& f, const char* name) {
   return true;
 }
 
+void drv_load_once();
+std::once_flag g_drv_once;
 bool drv_load(std::string* err) {
-  if (g_drv.tried) {
-    if (!g_drv.ok) *err = "CUDA driver multicast entry points unavailable";
-    return g_drv.ok;
-  }
+  std::call_once(g_drv_once, drv_load_once);
+  if (!g_drv.ok) *err = "CUDA driver multicast entry points unavailable";
+  return g_drv.ok;
+}
+
+void drv_load_once() {
   g_drv.tried = true;
   bool ok = bind_sym(g_drv.DeviceGet, "cuDeviceGet") &&
             bind_sym(g_drv.DeviceGetAttribute, "cuDeviceGetAttribute") &&
@@ -96,8 +101,6 @@ bool drv_load(std::string* err) {
             bind_sym(g_drv.MemImportFromShareableHandle, "cuMemImportFromShareableHandle") &&
             bind_sym(g_drv.GetErrorString, "cuGetErrorString");
   g_drv.ok = ok;
-  if (!ok) *err = "CUDA driver multicast entry points unavailable";
-  return ok;
 }
 
 std::string cu_err(CUresult r, const char* what) {

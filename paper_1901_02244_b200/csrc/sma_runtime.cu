@@ -21,6 +21,7 @@
 #include <unistd.h>
 
 #include <cmath>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -84,8 +85,14 @@ struct NcclApi {
 };
 NcclApi g_nccl;
 
+bool nccl_load_once();
+std::once_flag g_nccl_once;
 bool nccl_load() {
-  if (g_nccl.tried) return g_nccl.ok;
+  std::call_once(g_nccl_once, [] { nccl_load_once(); });
+  return g_nccl.ok;
+}
+
+bool nccl_load_once() {
   g_nccl.tried = true;
   void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
   if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
