@@ -236,11 +236,11 @@ def main():
     if args.zsync == "nvls" and collective:
         flags |= sma.FLAG_NVLS_ZSYNC
 
-    nccl_id = None
-    if world > 1:
-        obj = [sma.sma_nccl_unique_id() if rank == 0 else None]
+    nccl_id = nccl_id_a = None
+    if world > 1:   # one NCCL id per libsma communicator (the bench may create two)
+        obj = [(sma.sma_nccl_unique_id(), sma.sma_nccl_unique_id()) if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+        nccl_id, nccl_id_a = obj[0]
 
     w0 = sma_inputs.w0(d) if not learner else \
         np.random.default_rng(6).normal(0, 0.05 if args.config == "MLP" else 0.0, d).astype(np.float32)
@@ -317,6 +317,38 @@ def main():
     else:
         ms_max, launches_total = ms, launches
     kern_avg = phase_avg[0]
+
+    # ---------------------------------------------- clean NVLink measurement
+    # In Mode B the collectives overlap the replica kernel, so their event
+    # times include contention.  For N > 1 a second, Mode-A handle (same
+    # workload) runs a short serial pass: its reduce-scatter / all-gather times
+    # give the uncontended NVLink bus bandwidth (nccl-tests convention).
+    serial = None
+    if collective and mode == "B" and args.zsync == "nccl":
+        hA = sma.Sma(d, k, alpha, gamma, mu, w0, rank=rank, world=world, device=local,
+                     nccl_id=nccl_id_a, flags=(flags & ~sma.FLAG_OVERLAP))
+        hA.synth_grads(0, sma_inputs.SEED_G, stream)
+        for _ in range(5):
+            hA.step(stream)
+        barrier()
+        for ph in range(5):
+            hA.kernel_time(reset=True, phase=ph)
+        ns = max(10, args.steps // 4)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ns):
+            hA.step(stream)
+        e1.record(stream)
+        barrier()
+        pa = []
+        for ph in range(4):
+            pm, pn = hA.kernel_time(reset=True, phase=ph)
+            pa.append(pm / pn if pn else 0.0)
+        ta = torch.tensor([e0.elapsed_time(e1) / ns, *pa], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(ta, op=dist.ReduceOp.MAX)
+        serial = [float(x) for x in ta]
+        hA.close()
 
     # ------------------------------------------------------------------ e2e
     e2e = None
@@ -411,6 +443,15 @@ def main():
                         "times from CUDA events around each NCCL call on its stream, max over "
                         "ranks" + ("; in Mode B they run concurrently with the replica kernel"
                                    if mode == "B" else "")}
+            if serial is not None:
+                s_rs, s_ag = serial[2], serial[4]
+                s_comb = (2 * one / ((s_rs + s_ag) * 1e-3) / 1e9) if s_rs + s_ag > 0 else None
+                line["nvlink"]["serial_mode_a"] = {
+                    "ms_per_round": serial[0], "replica_ms": serial[1],
+                    "reduce_scatter_ms": s_rs, "shard_update_ms": serial[3],
+                    "all_gather_ms": s_ag, "rs_bus_gbs": bus(s_rs), "ag_bus_gbs": bus(s_ag),
+                    "bus_gbs": s_comb, "frac": (s_comb / NVLINK_PEAK_GBS) if s_comb else None,
+                    "note": "separate Mode-A handle, same workload, collectives not overlapped"}
         if e2e:
             line["e2e"] = e2e
         if args.tau != 1:
