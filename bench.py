@@ -157,7 +157,9 @@ def run_reference(args):
     alpha, gamma, mu = float(np.float32(1 / k)), float(np.float32(0.1)), float(np.float32(0.9))
     import oracle
     oracle.build()
-    n_idx = min(d, 1 << 20)   # bounded sample per step (~0.3 s of CPU per step at C4)
+    # bounded sample per step, sized so the whole run stays near a minute of CPU:
+    # 2^20 indices (~0.3 s per step at C4) for up to ~100 steps, fewer beyond
+    n_idx = min(d, max(1 << 14, min(1 << 20, (1 << 20) * 100 // max(1, args.steps + args.warmup))))
     rng = np.random.default_rng(1)
     idx = np.sort(rng.choice(d, n_idx, replace=False)) if n_idx < d else np.arange(d)
     state = oracle.State.init(sma_inputs.w0(d, idx=idx).astype(np.float64), k)
