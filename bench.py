@@ -392,8 +392,8 @@ def main():
         else:
             alg_bytes = 4 * d_pad * (3 * r + 2)
             kname = f"replica_step_{kvar}<kPartial{mode}>"
-        if args.matc:
-            alg_bytes = 4 * d_pad * (6 * r + (3 if mode == "fused" else 2))
+        if args.matc:   # replica kernel: r x (read w, g; write w, c) + z; reduce: r x read c
+            alg_bytes = 4 * d_pad * (5 * r + (4 if mode == "fused" else 2))
         if args.tau != 1 and not learner:   # mix of sync rounds and local-only iterations
             n_sync = (args.steps // args.tau) if args.tau > 1 else 0
             alg_bytes = (n_sync * alg_bytes + (args.steps - n_sync) * 4 * d_pad * 3 * r) / args.steps

@@ -72,7 +72,8 @@ enum {
     SMA_FLAG_OVERLAP = 1u,
     /* North_star-literal variant: the replica kernel writes every c_j to HBM
      * and a separate warp-shuffle/block-tree kernel reduces them.
-     * Moves 4 d_pad (6r+1) bytes per round instead of 4 d_pad (3r+2). */
+     * Moves 4 d_pad (5r+4) bytes per round instead of 4 d_pad (3r+3) at n = 1
+     * (5r+2 instead of 3r+2 on the collective path). */
     SMA_FLAG_MATERIALIZE_C = 2u,
     /* Record a device flag when any updated value is not finite; sma_step then
      * returns SMA_ERR_NONFINITE at the NEXT call that synchronises
