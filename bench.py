@@ -57,8 +57,9 @@ def parse():
     ap.add_argument("--ldg", action="store_true", help="force the direct-load replica kernel")
     ap.add_argument("--matc", action="store_true", help="north_star-literal c_j materialisation")
     ap.add_argument("--force-collective", action="store_true")
-    ap.add_argument("--zsync", choices=["nccl", "nvls"], default="nccl",
-                    help="inter-GPU z-sync: NCCL RS/AG (default) or the fused multicast kernel")
+    ap.add_argument("--zsync", choices=["nccl", "nvls", "p2p"], default="nccl",
+                    help="inter-GPU z-sync: NCCL RS/AG (default), or one fused kernel over "
+                         "NVSwitch multicast (nvls) / IPC-mapped peer memory (p2p)")
     ap.add_argument("--tau", type=int, default=1,
                     help="synchronise every tau iterations (sma_step_local on the others; "
                          "0 = never: the paper's 'no synchronisation' point, fig:overhead)")
@@ -238,6 +239,8 @@ def main():
         flags |= sma.FLAG_MATERIALIZE_C
     if args.zsync == "nvls" and collective:
         flags |= sma.FLAG_NVLS_ZSYNC
+    if args.zsync == "p2p" and collective:
+        flags |= sma.FLAG_P2P_ZSYNC
 
     nccl_id = nccl_id_a = None
     if world > 1:   # one NCCL id per libsma communicator (the bench may create two)
@@ -249,6 +252,10 @@ def main():
         np.random.default_rng(6).normal(0, 0.05 if args.config == "MLP" else 0.0, d).astype(np.float32)
     h = sma.Sma(d, k, alpha, gamma, mu, w0, rank=rank, world=world, device=local,
                 nccl_id=nccl_id, flags=flags)
+    if (flags & sma.FLAG_P2P_ZSYNC) and world > 1:   # map every rank's buffers (CUDA IPC)
+        handles = [None] * world
+        dist.all_gather_object(handles, sma.sma_p2p_handle(h.h))
+        sma.sma_p2p_connect(h.h, handles)
     r = h.local_count
     stream = torch.cuda.Stream()
     rnd = [0]

@@ -46,6 +46,7 @@ extern "C" {
 #define SMA_ABI_VERSION 1
 #define SMA_MAX_LOCAL_REPLICAS 64   /* r = replicas per GPU, P:1193-1194 ("m") */
 #define SMA_NCCL_ID_BYTES 128
+#define SMA_P2P_HANDLE_BYTES 64  /* cudaIpcMemHandle_t */
 
 typedef struct sma_handle sma_handle;   /* opaque; owns all device state */
 
@@ -101,7 +102,16 @@ enum {
      * multimem.st), with device-side barriers, instead of NCCL RS/AG.  Needs a
      * device with CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED; sma_create fails with
      * SMA_ERR_CUDA otherwise.  Collective path only. */
-    SMA_FLAG_NVLS_ZSYNC = 256u
+    SMA_FLAG_NVLS_ZSYNC = 256u,
+    /* The inter-GPU z-sync (reduce-scatter + shard update + all-gather) as ONE
+     * kernel over peer memory: every rank maps the others' [partial | z]
+     * buffers with CUDA IPC and, for its shard, loads the partials of all ranks,
+     * updates, and stores the result into every rank's z.  No NCCL is used (no
+     * nccl_id needed): after sma_create each rank exports sma_p2p_handle(), the
+     * caller all-gathers the handles and every rank calls sma_p2p_connect()
+     * before its first sma_step.  Several ranks may share one GPU.
+     * Collective path only; exclusive with SMA_FLAG_NVLS_ZSYNC. */
+    SMA_FLAG_P2P_ZSYNC = 512u
 };
 
 typedef struct {
@@ -114,7 +124,8 @@ typedef struct {
     int32_t  world;      /* number of GPUs n, >= 1; replicas are block-split over ranks      */
     int32_t  device;     /* CUDA device ordinal used by this rank                           */
     const void* nccl_id; /* SMA_NCCL_ID_BYTES from sma_nccl_unique_id() on rank 0, the same
-                            bytes on every rank; required iff world > 1 (copied)            */
+                            bytes on every rank; required iff world > 1 and not
+                            SMA_FLAG_P2P_ZSYNC (copied)                                     */
     uint32_t flags;      /* SMA_FLAG_* */
 } sma_config;
 
@@ -298,6 +309,19 @@ sma_status sma_plan_batch_indices(int64_t n_samples, int32_t k, int32_t batch,
                                   uint64_t batch_seed, int64_t round, int32_t j,
                                   int64_t* out);
 
+/* ------------------------------------------------------- P2P bootstrap */
+
+/* SMA_FLAG_P2P_ZSYNC: write this rank's SMA_P2P_HANDLE_BYTES IPC handle of its
+ * [flags | partial | z] region to out (host memory).  Errors: STATE (not a P2P
+ * handle), CUDA. */
+sma_status sma_p2p_handle(sma_handle* h, void* out);
+
+/* SMA_FLAG_P2P_ZSYNC: map the other ranks' regions.  handles: world x
+ * SMA_P2P_HANDLE_BYTES, in rank order (this rank's own entry is ignored).  Call
+ * once on every rank before the first sma_step.  Errors: STATE (not a P2P
+ * handle, or already connected), INVALID_ARG, CUDA. */
+sma_status sma_p2p_connect(sma_handle* h, const void* handles);
+
 /* ------------------------------------------------------------- utilities */
 
 /* Write a fresh NCCL unique id (SMA_NCCL_ID_BYTES) to out (rank 0 only;
@@ -311,10 +335,12 @@ sma_status sma_nccl_unique_id(void* out);
  *   SMA_PHASE_REDUCE_SCATTER ncclReduceScatter of the per-GPU partial (a6)
  *   SMA_PHASE_SHARD_UPDATE   the shard update kernel (a7, collective path)
  *   SMA_PHASE_ALL_GATHER     ncclAllGather of z (a8)
- *   SMA_PHASE_NVLS_ZSYNC     the fused multicast z-sync kernel (a6-a8, SMA_FLAG_NVLS_ZSYNC)
+ *   SMA_PHASE_FUSED_ZSYNC    the fused z-sync kernel (a6-a8; SMA_FLAG_NVLS_ZSYNC or
+ *                            SMA_FLAG_P2P_ZSYNC; also named SMA_PHASE_NVLS_ZSYNC)
  * Errors: INVALID_ARG (phase out of range). */
 enum { SMA_PHASE_REPLICA = 0, SMA_PHASE_REDUCE_SCATTER = 1, SMA_PHASE_SHARD_UPDATE = 2,
-       SMA_PHASE_ALL_GATHER = 3, SMA_PHASE_NVLS_ZSYNC = 4, SMA_NUM_PHASES = 5 };
+       SMA_PHASE_ALL_GATHER = 3, SMA_PHASE_NVLS_ZSYNC = 4, SMA_PHASE_FUSED_ZSYNC = 4,
+       SMA_NUM_PHASES = 5 };
 sma_status sma_kernel_time(sma_handle* h, int32_t phase, double* total_ms, int64_t* launches,
                            int reset);
 

@@ -115,4 +115,20 @@ bool nvls_setup(NvlsRegion* R, int device, int rank, int world, size_t bytes, co
 void nvls_teardown(NvlsRegion* R);
 cudaError_t launch_zsync_nvls(int mode, const NvlsArgs& a, int num_ctas, cudaStream_t s);
 
+// ----------------------------------------------------------------- P2P z-sync
+// (sma_p2p.cu) One cudaMalloc region per rank [flags (4 KB) | partial(s) | z[2]],
+// mapped into every rank's address space with CUDA IPC.  base[g] is rank g's
+// region as seen from this process; all offsets are in bytes.
+constexpr int kMaxP2PRanks = 64;
+struct P2PArgs {
+  char* base[kMaxP2PRanks];
+  int64_t off_flags, off_part, off_z, off_zprev;
+  int64_t off4, len4;    // this rank's shard in float4 chunks
+  float alpha, mu, coef_b;
+  int n, rank;
+  unsigned* ctl;         // local: [0] barrier-A target, [1] barrier-B target, [2] CTA counter
+  int* nonfinite;
+};
+cudaError_t launch_zsync_p2p(int mode, const P2PArgs& a, int num_ctas, cudaStream_t s);
+
 }  // namespace sma

@@ -1,0 +1,142 @@
+// sma_p2p.cu -- the inter-GPU z-sync (a6 + a7 + a8) as ONE kernel over peer
+// memory (CUDA IPC mappings of every rank's buffers), no NCCL on the data path.
+//
+// Every rank owns one cudaMalloc region [flags | partial(s) | z[2]] and maps the
+// regions of all other ranks (cudaIpcOpenMemHandle; handles exchanged by the
+// caller, e.g. with torch.distributed).  Rank g then, for each float4 chunk of
+// ITS shard of z:
+//   S  = sum over ranks g' = 0..n-1 (ascending) of partial_{g'}[chunk]   (a6: peer loads)
+//   z' = z + S + mu (z - z_prev)                 (Mode A)                 (a7)
+//   z' = (z + alpha S) + (mu - alpha k)(z - z_prev)  (Mode B)
+//   store z' into z[1-cur][chunk] of every rank                          (a8: peer stores)
+// so the reduce-scatter, the shard update and the all-gather are one pass that
+// overlaps loads from peers with stores to peers tile by tile.  Two barriers
+// (release stores of a per-source flag into every peer's flag array, acquire
+// spins on the local array; targets kept in device memory so CUDA graphs can
+// replay the kernel) order "every partial is complete" before the loads and
+// "every shard has landed" before the next round.  A barrier that does not
+// complete within ~30 s traps, so a broken peer fails the process loudly.
+//
+// Because no NCCL communicator is involved, several processes may share one
+// GPU (cudaIpc works within a device), which is how the multi-rank path is
+// tested on a single B200 (tests/test_p2p_multiprocess.py).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "sma_internal.h"
+
+namespace sma {
+namespace {
+constexpr int kP2PThreads = 256;
+
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Wait until flags[0..n) (written by the n ranks) all reached `target`.
+__device__ __forceinline__ void wait_all(const unsigned* flags, int n, unsigned target) {
+  const long long t0 = clock64();
+  for (int g = 0; g < n; ++g)
+    while ((int)(ld_acquire_sys(flags + g) - target) < 0) {
+      if (clock64() - t0 > 60000000000ll) __trap();  // ~30 s: a peer never arrived
+      __nanosleep(64);
+    }
+}
+__device__ __forceinline__ float4 ld_cg4(const float* p) {  // bypass L1: peer data
+  float4 v;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st_cg4(float* p, float4 v) {
+  asm volatile("st.global.cg.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+template <int MODE>
+__device__ __forceinline__ float4 shard_update(float4 zc, float4 s, float4 zp, const P2PArgs& a) {
+  float4 zn;
+  if (MODE == kPartialA) {  // z' = (z + S) + mu (z - z_prev)
+    zn.x = __fadd_rn(__fadd_rn(zc.x, s.x), __fmul_rn(a.mu, __fsub_rn(zc.x, zp.x)));
+    zn.y = __fadd_rn(__fadd_rn(zc.y, s.y), __fmul_rn(a.mu, __fsub_rn(zc.y, zp.y)));
+    zn.z = __fadd_rn(__fadd_rn(zc.z, s.z), __fmul_rn(a.mu, __fsub_rn(zc.z, zp.z)));
+    zn.w = __fadd_rn(__fadd_rn(zc.w, s.w), __fmul_rn(a.mu, __fsub_rn(zc.w, zp.w)));
+  } else {                  // z' = (z + alpha S) + (mu - alpha k)(z - z_prev)
+    zn.x = __fadd_rn(__fmaf_rn(a.alpha, s.x, zc.x), __fmul_rn(a.coef_b, __fsub_rn(zc.x, zp.x)));
+    zn.y = __fadd_rn(__fmaf_rn(a.alpha, s.y, zc.y), __fmul_rn(a.coef_b, __fsub_rn(zc.y, zp.y)));
+    zn.z = __fadd_rn(__fmaf_rn(a.alpha, s.z, zc.z), __fmul_rn(a.coef_b, __fsub_rn(zc.z, zp.z)));
+    zn.w = __fadd_rn(__fmaf_rn(a.alpha, s.w, zc.w), __fmul_rn(a.coef_b, __fsub_rn(zc.w, zp.w)));
+  }
+  return zn;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a) {
+  __shared__ unsigned s_targetA;
+  const int n = a.n;
+  if (threadIdx.x == 0) {
+    const unsigned tA = a.ctl[0] + 1u;
+    if (blockIdx.x == 0)  // barrier A: my partial is complete -> tell every rank
+      for (int g = 0; g < n; ++g)
+        st_release_sys(reinterpret_cast<unsigned*>(a.base[g] + a.off_flags) + a.rank, tA);
+    wait_all(reinterpret_cast<const unsigned*>(a.base[a.rank] + a.off_flags), n, tA);
+    s_targetA = tA;
+  }
+  __syncthreads();
+  bool bad = false;
+  const int64_t stride = (int64_t)gridDim.x * kP2PThreads;
+  for (int64_t c = (int64_t)blockIdx.x * kP2PThreads + threadIdx.x; c < a.len4; c += stride) {
+    const int64_t e = (a.off4 + c) << 2;  // element offset in the padded vector
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int g = 0; g < n; ++g) {  // a6: the shard's sum over ranks, ascending rank
+      const float4 v = ld_cg4(reinterpret_cast<const float*>(a.base[g] + a.off_part) + e);
+      s.x = __fadd_rn(s.x, v.x);
+      s.y = __fadd_rn(s.y, v.y);
+      s.z = __fadd_rn(s.z, v.z);
+      s.w = __fadd_rn(s.w, v.w);
+    }
+    const float* zl = reinterpret_cast<const float*>(a.base[a.rank] + a.off_z);
+    const float* zpl = reinterpret_cast<const float*>(a.base[a.rank] + a.off_zprev);
+    const float4 zn = shard_update<MODE>(ld_cg4(zl + e), s, ld_cg4(zpl + e), a);   // a7
+    for (int g = 0; g < n; ++g)  // a8: broadcast the updated shard chunk
+      st_cg4(reinterpret_cast<float*>(a.base[g] + a.off_zprev) + e, zn);
+    bad |= !(isfinite(zn.x) && isfinite(zn.y) && isfinite(zn.z) && isfinite(zn.w));
+  }
+  if (a.nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.nonfinite, 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();  // my peer stores before my arrival
+    const unsigned prev = atomicAdd(a.ctl + 2, 1u);
+    if (prev == gridDim.x - 1) {  // the last CTA of this rank closes the round
+      __threadfence_system();
+      a.ctl[2] = 0;
+      const unsigned tB = a.ctl[1] + 1u;
+      for (int g = 0; g < n; ++g)  // barrier B: my shard has landed everywhere
+        st_release_sys(reinterpret_cast<unsigned*>(a.base[g] + a.off_flags) + 64 + a.rank, tB);
+      wait_all(reinterpret_cast<const unsigned*>(a.base[a.rank] + a.off_flags) + 64, n, tB);
+      a.ctl[0] = s_targetA;
+      a.ctl[1] = tB;
+      __threadfence();
+    }
+  }
+}
+}  // namespace
+
+cudaError_t launch_zsync_p2p(int mode, const P2PArgs& a, int num_ctas, cudaStream_t s) {
+  const int64_t want = (a.len4 + kP2PThreads - 1) / kP2PThreads;
+  int grid = (int)(want < num_ctas ? want : num_ctas);
+  if (grid < 1) grid = 1;
+  if (mode == kPartialA)
+    zsync_p2p_kernel<kPartialA><<<grid, kP2PThreads, 0, s>>>(a);
+  else
+    zsync_p2p_kernel<kPartialB><<<grid, kP2PThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace sma

@@ -245,6 +245,12 @@ struct sma_handle {
   NvlsRegion nv;
   size_t nv_off_part = 0, nv_off_z = 0;
   unsigned* nv_ctl = nullptr;  // [0..1] expect, [2] done counter (local memory)
+  // P2P z-sync (CUDA IPC)
+  bool p2p = false, p2p_connected = false;
+  char* p2p_region = nullptr;
+  size_t p2p_off_part = 0, p2p_off_z = 0;
+  std::vector<char*> p2p_base;  // per rank, as mapped in this process
+  unsigned* p2p_ctl = nullptr;
   cudaStream_t sB = nullptr, sIO = nullptr;
   cudaEvent_t evFork = nullptr, evJoin = nullptr, evDone = nullptr;
   bool any_work = false;
@@ -303,6 +309,15 @@ void free_all(sma_handle* h) {
   if (h->any_work) cudaDeviceSynchronize();
   for (int i = 0; i < 2; ++i)
     if (h->gexec[i]) cudaGraphExecDestroy(h->gexec[i]);
+  if (h->p2p) {
+    for (int g = 0; g < (int)h->p2p_base.size(); ++g)
+      if (g != h->cfg.rank && h->p2p_base[g]) cudaIpcCloseMemHandle(h->p2p_base[g]);
+    cudaFree(h->p2p_region);
+    cudaFree(h->p2p_ctl);
+    h->zbuf = nullptr;
+    h->P = nullptr;
+    h->Q = nullptr;
+  }
   if (h->nvls) nvls_teardown(&h->nv);
   cudaFree(h->nv_ctl);
   if (h->nvls) {  // these live in the NVLS region, not in cudaMalloc memory
@@ -438,6 +453,29 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
                          cudaStream_t s) {
   const size_t cnt = (size_t)h->shard_len;
   cudaEvent_t* tp = nullptr;
+  if (h->p2p) {  // a6-a8 in one kernel over IPC-mapped peer memory
+    P2PArgs a{};
+    for (int g = 0; g < h->cfg.world; ++g) a.base[g] = h->p2p_base[g];
+    a.off_flags = 0;
+    a.off_part = reinterpret_cast<const char*>(partial) - h->p2p_region;
+    a.off_z = reinterpret_cast<const char*>(h->z()) - h->p2p_region;
+    a.off_zprev = reinterpret_cast<const char*>(h->zprev()) - h->p2p_region;
+    a.off4 = h->shard_off / 4;
+    a.len4 = h->shard_len / 4;
+    a.alpha = h->alpha;
+    a.mu = h->mu;
+    a.coef_b = coef_b;
+    a.n = h->cfg.world;
+    a.rank = h->cfg.rank;
+    a.ctl = h->p2p_ctl;
+    a.nonfinite = h->check ? h->nonfinite : nullptr;
+    STATUS_TRY(timer_pair(h, SMA_PHASE_FUSED_ZSYNC, &tp));
+    if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
+    CUDA_TRY(launch_zsync_p2p(mode, a, h->overlap ? (h->sync_sms > 0 ? h->sync_sms : 1)
+                                                  : 2 * h->num_sms, s));
+    if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
+    return SMA_OK;
+  }
   if (h->nvls) {  // a6-a8 in one multicast kernel
     NvlsArgs a{};
     const size_t part_off = (size_t)(reinterpret_cast<const char*>(partial) -
@@ -553,6 +591,13 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
   h->graphs = (f & SMA_FLAG_CUDA_GRAPH) != 0 && !h->timing;
   h->check = (f & SMA_FLAG_CHECK_FINITE) != 0;
   h->nvls = (f & SMA_FLAG_NVLS_ZSYNC) != 0;
+  h->p2p = (f & SMA_FLAG_P2P_ZSYNC) != 0;
+  if (h->p2p && h->nvls)
+    return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_P2P_ZSYNC and SMA_FLAG_NVLS_ZSYNC are exclusive");
+  if (h->p2p && !h->collective)
+    return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_P2P_ZSYNC needs world > 1 or SMA_FLAG_FORCE_COLLECTIVE");
+  if (h->p2p && cfg->world > kMaxP2PRanks)
+    return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_P2P_ZSYNC supports at most %d ranks", kMaxP2PRanks);
   if (h->nvls && !h->collective)
     return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_NVLS_ZSYNC needs world > 1 or SMA_FLAG_FORCE_COLLECTIVE");
   h->d_pad = sma_plan_d_pad(cfg->d, cfg->world);
@@ -592,7 +637,7 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
   CUDA_TRY(cudaEventCreateWithFlags(&h->evJoin, cudaEventDisableTiming));
   CUDA_TRY(cudaEventCreateWithFlags(&h->evDone, cudaEventDisableTiming));
   const size_t dp = (size_t)h->d_pad;
-  if (h->collective) {  // the communicator first: the collective buffers come from NCCL
+  if (h->collective && !h->p2p) {  // the communicator first: the collective buffers come from NCCL
     if (!nccl_load()) return fail(SMA_ERR_NCCL, "cannot load NCCL: %s", g_nccl.why.c_str());
     ncclUniqueId id;
     if (cfg->world > 1) {
@@ -606,7 +651,24 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
     if (h->sync_sms > h->num_sms - 1) h->sync_sms = h->num_sms - 1;
   }
   STATUS_TRY(alloc_zero(&h->W, dp * (h->r > 0 ? h->r : 1)));
-  if (h->nvls) {
+  if (h->p2p) {
+    // [flags (4 KB) | P, or Q[2] | z[2]] in one IPC-exportable allocation
+    h->p2p_off_part = 4096;
+    h->p2p_off_z = h->p2p_off_part + sizeof(float) * dp * (h->overlap ? 2 : 1);
+    const size_t bytes = h->p2p_off_z + sizeof(float) * 2 * dp;
+    CUDA_TRY(cudaMalloc(&h->p2p_region, bytes));
+    CUDA_TRY(cudaMemset(h->p2p_region, 0, bytes));
+    h->zbuf = reinterpret_cast<float*>(h->p2p_region + h->p2p_off_z);
+    if (h->overlap)
+      h->Q = reinterpret_cast<float*>(h->p2p_region + h->p2p_off_part);
+    else
+      h->P = reinterpret_cast<float*>(h->p2p_region + h->p2p_off_part);
+    CUDA_TRY(cudaMalloc(&h->p2p_ctl, 4 * sizeof(unsigned)));
+    CUDA_TRY(cudaMemset(h->p2p_ctl, 0, 4 * sizeof(unsigned)));
+    h->p2p_base.assign(cfg->world, nullptr);
+    h->p2p_base[cfg->rank] = h->p2p_region;
+    h->p2p_connected = cfg->world == 1;  // a single rank maps only itself
+  } else if (h->nvls) {
     // [flags (4 KB) | P, or Q[2] | z[2]] bound to one multicast object per rank
     h->nv_off_part = 4096;
     h->nv_off_z = h->nv_off_part + sizeof(float) * dp * (h->overlap ? 2 : 1);
@@ -697,8 +759,8 @@ sma_status sma_create(const sma_config* cfg, const float* w0_host, sma_handle** 
     return fail(SMA_ERR_INVALID_ARG, "bad rank/world %d/%d", cfg->rank, cfg->world);
   if (!finite_f(cfg->alpha) || !finite_f(cfg->gamma) || !finite_f(cfg->mu))
     return fail(SMA_ERR_INVALID_ARG, "non-finite hyper-parameter");
-  if (cfg->world > 1 && !cfg->nccl_id)
-    return fail(SMA_ERR_INVALID_ARG, "world > 1 requires nccl_id");
+  if (cfg->world > 1 && !cfg->nccl_id && !(cfg->flags & SMA_FLAG_P2P_ZSYNC))
+    return fail(SMA_ERR_INVALID_ARG, "world > 1 requires nccl_id (or SMA_FLAG_P2P_ZSYNC)");
   sma_handle* h = new sma_handle();
   sma_status st = create_impl(cfg, w0_host, h);
   if (st != SMA_OK) {
@@ -755,6 +817,8 @@ sma_status sma_synth_grads(sma_handle* h, int64_t round, uint64_t seed, void* st
 
 sma_status sma_step(sma_handle* h, void* stream) {
   if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (h->p2p && !h->p2p_connected)
+    return fail(SMA_ERR_STATE, "SMA_FLAG_P2P_ZSYNC: call sma_p2p_connect on every rank first");
   for (int i = 0; i < h->r; ++i)
     if (!h->gptr[i])
       return fail(SMA_ERR_GRADS_MISSING, "learner %d has no registered gradient", h->j0 + i);
@@ -1139,6 +1203,43 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
   for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
   advance(h);
   return mark_done(h, s);
+}
+
+sma_status sma_p2p_handle(sma_handle* h, void* out) {
+  if (!h || !out) return fail(SMA_ERR_INVALID_ARG, "NULL argument");
+  if (!h->p2p) return fail(SMA_ERR_STATE, "not an SMA_FLAG_P2P_ZSYNC handle");
+  DeviceGuard guard(h->dev);
+  cudaIpcMemHandle_t ipc;
+  CUDA_TRY(cudaIpcGetMemHandle(&ipc, h->p2p_region));
+  static_assert(sizeof(ipc) == SMA_P2P_HANDLE_BYTES, "IPC handle size");
+  memcpy(out, &ipc, sizeof ipc);
+  return SMA_OK;
+}
+
+sma_status sma_p2p_connect(sma_handle* h, const void* handles) {
+  if (!h || !handles) return fail(SMA_ERR_INVALID_ARG, "NULL argument");
+  if (!h->p2p) return fail(SMA_ERR_STATE, "not an SMA_FLAG_P2P_ZSYNC handle");
+  if (h->p2p_connected) return fail(SMA_ERR_STATE, "already connected");
+  DeviceGuard guard(h->dev);
+  const char* all = static_cast<const char*>(handles);
+  for (int g = 0; g < h->cfg.world; ++g) {
+    if (g == h->cfg.rank) continue;
+    cudaIpcMemHandle_t ipc;
+    memcpy(&ipc, all + (size_t)g * SMA_P2P_HANDLE_BYTES, sizeof ipc);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, ipc, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      for (int q = 0; q < g; ++q)
+        if (q != h->cfg.rank && h->p2p_base[q]) {
+          cudaIpcCloseMemHandle(h->p2p_base[q]);
+          h->p2p_base[q] = nullptr;
+        }
+      return fail(SMA_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d) failed: %s", g, cudaGetErrorString(e));
+    }
+    h->p2p_base[g] = static_cast<char*>(p);
+  }
+  h->p2p_connected = true;
+  return SMA_OK;
 }
 
 sma_status sma_kernel_time(sma_handle* h, int32_t phase, double* total_ms, int64_t* launches,

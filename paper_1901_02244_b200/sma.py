@@ -25,6 +25,8 @@ FLAG_TIMING = 32
 FLAG_KERNEL_TMA = 64
 FLAG_KERNEL_LDG = 128
 FLAG_NVLS_ZSYNC = 256
+FLAG_P2P_ZSYNC = 512
+P2P_HANDLE_BYTES = 64
 MAX_LOCAL_REPLICAS = 64
 NCCL_ID_BYTES = 128
 
@@ -41,7 +43,8 @@ EXPORTS = ["sma_create", "sma_destroy", "sma_set_learner_grads", "sma_set_learne
            "sma_plan_replica_location", "sma_plan_local_replicas", "sma_plan_shard_range",
            "sma_plan_batch_indices", "sma_nccl_unique_id", "sma_kernel_time",
            "sma_launch_count", "sma_info", "sma_last_error", "sma_abi_version",
-           "sma_step_local", "sma_autotune_step", "sma_set_local_replicas", "sma_learner_step"]
+           "sma_step_local", "sma_autotune_step", "sma_set_local_replicas", "sma_learner_step",
+           "sma_p2p_handle", "sma_p2p_connect"]
 
 
 class SmaError(RuntimeError):
@@ -104,6 +107,8 @@ def load():
         "sma_autotune_step": ([i32, C.c_double, P, P, P], st),
         "sma_set_local_replicas": ([P, i32, P], st),
         "sma_learner_step": ([P, i64, P], st),
+        "sma_p2p_handle": ([P, P], st),
+        "sma_p2p_connect": ([P, P], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -241,6 +246,18 @@ def sma_learner_grads(h: int, rnd: int, stream=None) -> None:
 
 def sma_learner_step(h: int, rnd: int, stream=None) -> None:
     _check(load().sma_learner_step(h, rnd, _stream(stream)), "sma_learner_step")
+
+
+def sma_p2p_handle(h: int) -> bytes:
+    buf = (C.c_char * P2P_HANDLE_BYTES)()
+    _check(load().sma_p2p_handle(h, buf), "sma_p2p_handle")
+    return bytes(buf)
+
+
+def sma_p2p_connect(h: int, handles: list) -> None:
+    blob = b"".join(bytes(x) for x in handles)
+    buf = C.create_string_buffer(blob, len(blob))
+    _check(load().sma_p2p_connect(h, buf), "sma_p2p_connect")
 
 
 def sma_plan_d_pad(d: int, world: int) -> int:

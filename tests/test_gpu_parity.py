@@ -53,6 +53,10 @@ COLLECTIVE_FLAGS = {
     "nvlsA_matc": 16 | 2 | 256,
     "nvlsB": 16 | 1 | 256,
     "nvlsB_graph": 16 | 1 | 8 | 256,
+    "p2pA": 16 | 512,
+    "p2pA_matc": 16 | 2 | 512,
+    "p2pB": 16 | 1 | 512,
+    "p2pB_graph": 16 | 1 | 8 | 512,
 }
 
 
@@ -554,7 +558,7 @@ def test_randomized_configs(torch_cuda, S, orc):
     vs the oracle: catches size/alignment/replica-count corner cases (d % 4,
     r not a multiple of the load batch, tiny d, r = 1)."""
     rng = np.random.default_rng(2024)
-    variants = [0, 2, 8, 64, 128, 16, 16 | 1, 16 | 2, 16 | 1 | 8, 16 | 64]
+    variants = [0, 2, 8, 64, 128, 16, 16 | 1, 16 | 2, 16 | 1 | 8, 16 | 64, 16 | 512, 16 | 1 | 512]
     s = torch_cuda.cuda.Stream()
     for trial in range(30):
         d = int(rng.choice([1, 2, 3, 5, 63, 64, 65, 511, 513, 2047, 2049, 4099, 12345,
