@@ -57,9 +57,10 @@ def parse():
     ap.add_argument("--ldg", action="store_true", help="force the direct-load replica kernel")
     ap.add_argument("--matc", action="store_true", help="north_star-literal c_j materialisation")
     ap.add_argument("--force-collective", action="store_true")
-    ap.add_argument("--zsync", choices=["nccl", "nvls", "p2p"], default="nccl",
-                    help="inter-GPU z-sync: NCCL RS/AG (default), or one fused kernel over "
-                         "NVSwitch multicast (nvls) / IPC-mapped peer memory (p2p)")
+    ap.add_argument("--zsync", choices=["auto", "nccl", "nvls", "p2p"], default="auto",
+                    help="inter-GPU z-sync: one fused kernel over IPC-mapped peer memory (p2p), "
+                         "NCCL RS/AG (nccl), or one fused kernel over NVSwitch multicast (nvls); "
+                         "auto = p2p, falling back to nccl if the peer mapping cannot be set up")
     ap.add_argument("--tau", type=int, default=1,
                     help="synchronise every tau iterations (sma_step_local on the others; "
                          "0 = never: the paper's 'no synchronisation' point, fig:overhead)")
@@ -239,7 +240,7 @@ def main():
         flags |= sma.FLAG_MATERIALIZE_C
     if args.zsync == "nvls" and collective:
         flags |= sma.FLAG_NVLS_ZSYNC
-    if args.zsync == "p2p" and collective:
+    if args.zsync in ("p2p", "auto") and collective:
         flags |= sma.FLAG_P2P_ZSYNC
 
     nccl_id = nccl_id_a = None
@@ -250,12 +251,36 @@ def main():
 
     w0 = sma_inputs.w0(d) if not learner else \
         np.random.default_rng(6).normal(0, 0.05 if args.config == "MLP" else 0.0, d).astype(np.float32)
-    h = sma.Sma(d, k, alpha, gamma, mu, w0, rank=rank, world=world, device=local,
-                nccl_id=nccl_id, flags=flags)
-    if (flags & sma.FLAG_P2P_ZSYNC) and world > 1:   # map every rank's buffers (CUDA IPC)
-        handles = [None] * world
-        dist.all_gather_object(handles, sma.sma_p2p_handle(h.h))
-        sma.sma_p2p_connect(h.h, handles)
+    def make_handle(fl):
+        hh = sma.Sma(d, k, alpha, gamma, mu, w0, rank=rank, world=world, device=local,
+                     nccl_id=nccl_id, flags=fl)
+        if (fl & sma.FLAG_P2P_ZSYNC) and world > 1:   # map every rank's buffers (CUDA IPC)
+            handles = [None] * world
+            dist.all_gather_object(handles, sma.sma_p2p_handle(hh.h))
+            sma.sma_p2p_connect(hh.h, handles)
+        return hh
+
+    zsync = args.zsync if args.zsync != "auto" else ("p2p" if collective else "none")
+    if args.zsync == "auto" and world > 1:
+        # every rank must take the same path: agree on whether the peer mapping worked
+        ok, h, err = 1, None, ""
+        try:
+            h = make_handle(flags)
+        except Exception as e:  # noqa: BLE001 -- any setup failure selects NCCL
+            ok, err = 0, str(e)
+        flag_t = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag_t, op=dist.ReduceOp.MIN)
+        if int(flag_t[0]) == 0:
+            if h is not None:
+                h.close()
+            if rank == 0:
+                print(f"p2p z-sync unavailable ({err or 'on another rank'}); using NCCL",
+                      file=sys.stderr, flush=True)
+            flags &= ~sma.FLAG_P2P_ZSYNC
+            zsync = "nccl"
+            h = make_handle(flags)
+    else:
+        h = make_handle(flags)
     r = h.local_count
     stream = torch.cuda.Stream()
     rnd = [0]
@@ -334,9 +359,10 @@ def main():
     # workload) runs a short serial pass: its reduce-scatter / all-gather times
     # give the uncontended NVLink bus bandwidth (nccl-tests convention).
     serial = None
-    if collective and mode == "B" and args.zsync == "nccl":
-        hA = sma.Sma(d, k, alpha, gamma, mu, w0, rank=rank, world=world, device=local,
-                     nccl_id=nccl_id_a, flags=(flags & ~sma.FLAG_OVERLAP))
+    if collective and mode == "B" and zsync in ("nccl", "p2p"):
+        nccl_id_main, nccl_id = nccl_id, nccl_id_a   # the second handle's own communicator
+        hA = make_handle(flags & ~sma.FLAG_OVERLAP)
+        nccl_id = nccl_id_main
         hA.synth_grads(0, sma_inputs.SEED_G, stream)
         for _ in range(5):
             hA.step(stream)
@@ -351,7 +377,7 @@ def main():
         e1.record(stream)
         barrier()
         pa = []
-        for ph in range(4):
+        for ph in range(5):
             pm, pn = hA.kernel_time(reset=True, phase=ph)
             pa.append(pm / pn if pn else 0.0)
         ta = torch.tensor([e0.elapsed_time(e1) / ns, *pa], dtype=torch.float64, device="cuda")
@@ -424,7 +450,7 @@ def main():
                        "mode": mode, "kernel": kvar,
                        "materialize_c": bool(args.matc),
                        "parallelism": f"sma-dp{world}" + ("" if not collective else
-                                                           f"+{args.zsync}-zsync"),
+                                                           f"+{zsync}-zsync"),
                        "l2": "no flush: per-round working set "
                              f"{(alg_bytes / 1e9):.2f} GB/GPU >> 126 MB L2"},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
@@ -439,13 +465,13 @@ def main():
             rs_ms, up_ms, ag_ms, nv_ms = phase_avg[1], phase_avg[2], phase_avg[3], phase_avg[4]
             bus = lambda ms_: (one / (ms_ * 1e-3) / 1e9) if ms_ > 0 else None  # noqa: E731
             comb = (2 * one / ((rs_ms + ag_ms) * 1e-3) / 1e9) if rs_ms + ag_ms > 0 else None
-            if nv_ms > 0:   # fused multicast kernel: same bus-byte convention over its time
+            if nv_ms > 0:   # fused z-sync kernel: same bus-byte convention over its time
                 comb = 2 * one / (nv_ms * 1e-3) / 1e9
             line["nvlink"] = {
                 "bus_bytes_per_gpu_per_round": 2 * one,
-                "zsync": args.zsync,
+                "zsync": zsync,
                 "reduce_scatter_ms": rs_ms, "shard_update_ms": up_ms, "all_gather_ms": ag_ms,
-                "nvls_zsync_ms": nv_ms,
+                "fused_zsync_ms": nv_ms,
                 "rs_bus_gbs": bus(rs_ms), "ag_bus_gbs": bus(ag_ms), "bus_gbs": comb,
                 "peak_gbs": NVLINK_PEAK_GBS,
                 "frac": (comb / NVLINK_PEAK_GBS) if comb else None,
@@ -454,14 +480,17 @@ def main():
                         "ranks" + ("; in Mode B they run concurrently with the replica kernel"
                                    if mode == "B" else "")}
             if serial is not None:
-                s_rs, s_ag = serial[2], serial[4]
+                s_rs, s_ag, s_fz = serial[2], serial[4], serial[5]
                 s_comb = (2 * one / ((s_rs + s_ag) * 1e-3) / 1e9) if s_rs + s_ag > 0 else None
+                if s_fz > 0:
+                    s_comb = 2 * one / (s_fz * 1e-3) / 1e9
                 line["nvlink"]["serial_mode_a"] = {
                     "ms_per_round": serial[0], "replica_ms": serial[1],
                     "reduce_scatter_ms": s_rs, "shard_update_ms": serial[3],
-                    "all_gather_ms": s_ag, "rs_bus_gbs": bus(s_rs), "ag_bus_gbs": bus(s_ag),
+                    "all_gather_ms": s_ag, "fused_zsync_ms": s_fz,
+                    "rs_bus_gbs": bus(s_rs), "ag_bus_gbs": bus(s_ag),
                     "bus_gbs": s_comb, "frac": (s_comb / NVLINK_PEAK_GBS) if s_comb else None,
-                    "note": "separate Mode-A handle, same workload, collectives not overlapped"}
+                    "note": "separate Mode-A handle, same workload, z-sync not overlapped"}
         if e2e:
             line["e2e"] = e2e
         if args.tau != 1:

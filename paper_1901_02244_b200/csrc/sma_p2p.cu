@@ -129,8 +129,11 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
 }  // namespace
 
 cudaError_t launch_zsync_p2p(int mode, const P2PArgs& a, int num_ctas, cudaStream_t s) {
+  // a full grid (one float4 chunk per thread: all n peer loads of a chunk in
+  // flight at once) unless the caller caps it; measured 2.9 TB/s with 2 CTAs/SM
+  // and a grid-stride loop at n = 1
   const int64_t want = (a.len4 + kP2PThreads - 1) / kP2PThreads;
-  int grid = (int)(want < num_ctas ? want : num_ctas);
+  int grid = (int)((num_ctas > 0 && want > num_ctas) ? num_ctas : want);
   if (grid < 1) grid = 1;
   if (mode == kPartialA)
     zsync_p2p_kernel<kPartialA><<<grid, kP2PThreads, 0, s>>>(a);

@@ -44,6 +44,10 @@ def _worker(rank, world, port, flags, d, k, R, out):
     a, g, m = (float(np.float32(x)) for x in (1 / k, 0.1, 0.9))
     h = sma.Sma(d, k, a, g, m, sma_inputs.w0(d), rank=rank, world=world, device=rank,
                 nccl_id=obj[0], flags=flags)
+    if flags & sma.FLAG_P2P_ZSYNC:
+        handles = [None] * world
+        dist.all_gather_object(handles, sma.sma_p2p_handle(h.h))
+        sma.sma_p2p_connect(h.h, handles)
     s = torch.cuda.Stream()
     for i in range(R):
         h.synth_grads(i, sma_inputs.SEED_G, s)
@@ -57,7 +61,7 @@ def _worker(rank, world, port, flags, d, k, R, out):
 
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("flags", [0, 1, 8, 1 | 8, 256, 1 | 256])
+@pytest.mark.parametrize("flags", [0, 1, 8, 1 | 8, 256, 1 | 256, 512, 1 | 512, 1 | 8 | 512])
 def test_multi_gpu_matches_oracle(orc, tmp_path, flags):
     import torch.multiprocessing as mp
 
