@@ -46,15 +46,27 @@ __device__ __forceinline__ void wait_all(const unsigned* flags, int n, unsigned 
       __nanosleep(64);
     }
 }
-__device__ __forceinline__ float4 ld_cg4(const float* p) {  // bypass L1: peer data
+// Partials and z[cur] are read-only for the whole kernel on every rank, so the
+// non-coherent path is legal for them (no L1 allocation: peer data is never
+// reused); z[1-cur] of this rank's chunk is read then written by the same
+// thread, so it uses the coherent path.  (.cg loads here measured ~half the
+// bandwidth at n = 1.)
+__device__ __forceinline__ float4 ld_ro4(const float* p) {
   float4 v;
-  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
                : "l"(p));
   return v;
 }
-__device__ __forceinline__ void st_cg4(float* p, float4 v) {
-  asm volatile("st.global.cg.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
+__device__ __forceinline__ float4 ld_rw4(const float* p) {
+  float4 v;
+  asm volatile("ld.global.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void st4(float* p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z),
                "f"(v.w)
                : "memory");
 }
@@ -91,21 +103,41 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
   __syncthreads();
   bool bad = false;
   const int64_t stride = (int64_t)gridDim.x * kP2PThreads;
-  for (int64_t c = (int64_t)blockIdx.x * kP2PThreads + threadIdx.x; c < a.len4; c += stride) {
-    const int64_t e = (a.off4 + c) << 2;  // element offset in the padded vector
-    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  const float* zl = reinterpret_cast<const float*>(a.base[a.rank] + a.off_z);
+  const float* zpl = reinterpret_cast<const float*>(a.base[a.rank] + a.off_zprev);
+  // two chunks per iteration: 2n peer loads + 4 local loads in flight
+  int64_t c = (int64_t)blockIdx.x * kP2PThreads + threadIdx.x;
+  for (; c + stride < a.len4; c += 2 * stride) {
+    const int64_t e0 = (a.off4 + c) << 2, e1 = (a.off4 + c + stride) << 2;
+    float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
     for (int g = 0; g < n; ++g) {  // a6: the shard's sum over ranks, ascending rank
-      const float4 v = ld_cg4(reinterpret_cast<const float*>(a.base[g] + a.off_part) + e);
-      s.x = __fadd_rn(s.x, v.x);
-      s.y = __fadd_rn(s.y, v.y);
-      s.z = __fadd_rn(s.z, v.z);
-      s.w = __fadd_rn(s.w, v.w);
+      const float* pg = reinterpret_cast<const float*>(a.base[g] + a.off_part);
+      const float4 v0 = ld_ro4(pg + e0), v1 = ld_ro4(pg + e1);
+      s0.x = __fadd_rn(s0.x, v0.x); s0.y = __fadd_rn(s0.y, v0.y);
+      s0.z = __fadd_rn(s0.z, v0.z); s0.w = __fadd_rn(s0.w, v0.w);
+      s1.x = __fadd_rn(s1.x, v1.x); s1.y = __fadd_rn(s1.y, v1.y);
+      s1.z = __fadd_rn(s1.z, v1.z); s1.w = __fadd_rn(s1.w, v1.w);
     }
-    const float* zl = reinterpret_cast<const float*>(a.base[a.rank] + a.off_z);
-    const float* zpl = reinterpret_cast<const float*>(a.base[a.rank] + a.off_zprev);
-    const float4 zn = shard_update<MODE>(ld_cg4(zl + e), s, ld_cg4(zpl + e), a);   // a7
-    for (int g = 0; g < n; ++g)  // a8: broadcast the updated shard chunk
-      st_cg4(reinterpret_cast<float*>(a.base[g] + a.off_zprev) + e, zn);
+    const float4 zn0 = shard_update<MODE>(ld_ro4(zl + e0), s0, ld_rw4(zpl + e0), a);  // a7
+    const float4 zn1 = shard_update<MODE>(ld_ro4(zl + e1), s1, ld_rw4(zpl + e1), a);
+    for (int g = 0; g < n; ++g) {  // a8: broadcast the updated shard chunks
+      float* zg = reinterpret_cast<float*>(a.base[g] + a.off_zprev);
+      st4(zg + e0, zn0);
+      st4(zg + e1, zn1);
+    }
+    bad |= !(isfinite(zn0.x) && isfinite(zn0.y) && isfinite(zn0.z) && isfinite(zn0.w));
+    bad |= !(isfinite(zn1.x) && isfinite(zn1.y) && isfinite(zn1.z) && isfinite(zn1.w));
+  }
+  for (; c < a.len4; c += stride) {
+    const int64_t e = (a.off4 + c) << 2;  // element offset in the padded vector
+    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int g = 0; g < n; ++g) {
+      const float4 v = ld_ro4(reinterpret_cast<const float*>(a.base[g] + a.off_part) + e);
+      sum.x = __fadd_rn(sum.x, v.x); sum.y = __fadd_rn(sum.y, v.y);
+      sum.z = __fadd_rn(sum.z, v.z); sum.w = __fadd_rn(sum.w, v.w);
+    }
+    const float4 zn = shard_update<MODE>(ld_ro4(zl + e), sum, ld_rw4(zpl + e), a);
+    for (int g = 0; g < n; ++g) st4(reinterpret_cast<float*>(a.base[g] + a.off_zprev) + e, zn);
     bad |= !(isfinite(zn.x) && isfinite(zn.y) && isfinite(zn.z) && isfinite(zn.w));
   }
   if (a.nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.nonfinite, 1);
@@ -129,9 +161,9 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
 }  // namespace
 
 cudaError_t launch_zsync_p2p(int mode, const P2PArgs& a, int num_ctas, cudaStream_t s) {
-  // a full grid (one float4 chunk per thread: all n peer loads of a chunk in
-  // flight at once) unless the caller caps it; measured 2.9 TB/s with 2 CTAs/SM
-  // and a grid-stride loop at n = 1
+  // A persistent grid (num_ctas: #SMs x 4): every CTA pays one system-scope
+  // acquire (barrier A) and one system fence + arrival (barrier B), so a full
+  // grid of ~25k CTAs spent more time in those than in moving data.
   const int64_t want = (a.len4 + kP2PThreads - 1) / kP2PThreads;
   int grid = (int)((num_ctas > 0 && want > num_ctas) ? num_ctas : want);
   if (grid < 1) grid = 1;

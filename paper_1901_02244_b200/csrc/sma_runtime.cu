@@ -471,7 +471,7 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
     a.nonfinite = h->check ? h->nonfinite : nullptr;
     STATUS_TRY(timer_pair(h, SMA_PHASE_FUSED_ZSYNC, &tp));
     if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
-    CUDA_TRY(launch_zsync_p2p(mode, a, 0, s));  // full grid; Mode B: high-priority stream
+    CUDA_TRY(launch_zsync_p2p(mode, a, 4 * h->num_sms, s));  // Mode B: high-priority stream
     if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
     return SMA_OK;
   }
