@@ -78,9 +78,11 @@ cudaError_t launch_softmax_round(const float* X, const int32_t* y, const int32_t
                                  float* G, const ReplicaArgs& a, cudaStream_t s);
 // MLP learner (kind 1) gradient for the r local replicas (sma_learner_mlp.cu).
 // A1: double-float scratch [r][b][hidden]; DA: fp32 scratch [r][b][hidden].
+// E: fp32 scratch [r][b][classes].
 cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* perm, int64_t pos0,
                             int b, int in_dim, int hidden, int classes, const float* W, int64_t ld,
-                            int r, int j0, float2* A1, float* DA, float* G, cudaStream_t s);
+                            int r, int j0, float2* A1, float* E, float* DA, float* G,
+                            cudaStream_t s);
 // Broadcast: dst rows [r][ld] := src [ld]   and   y := x   (restart / init).
 cudaError_t launch_broadcast_rows(float* dst, int64_t ld, int r, const float* src, int64_t n4,
                                   int num_sms, cudaStream_t s);

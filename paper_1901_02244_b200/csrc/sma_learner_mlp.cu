@@ -9,8 +9,9 @@
 //      not certain (R18: the ReLU mask is an integer decision, taken at
 //      fp64-level accuracy on both sides, so the GPU and the fp64 oracle agree
 //      on it except within ~1e-13 of a kink).
-//   2. mlp_head_kernel    grid (r): h = relu(a1) (fp32), logits, max-subtracted
-//      softmax, e = p - onehot, dW2 = e^T h / b, db2, da1 = (W2^T e) * [a1 > 0].
+//   2. mlp_logits_kernel  grid (r, b): h = relu(a1) (fp32), logits, max-subtracted
+//      softmax, e = p - onehot   ->  E
+//   2b. mlp_head_kernel   grid (r, 16): dW2 = e^T h / b, db2, da1 = (W2^T e) * [a1 > 0].
 //   3. mlp_w1_kernel      grid (r, hidden/16, in_dim/64): dW1 = da1^T X / b, db1.
 // fp32 FFMA elsewhere; no TF32.
 #include <cuda_runtime.h>
@@ -22,9 +23,9 @@
 namespace sma {
 namespace {
 constexpr int kUnits = 16;       // hidden units per CTA of the dW1 kernel
-constexpr int kHidUnits = 8;     // hidden units per CTA of the forward kernel
+constexpr int kHidUnits = 4;     // hidden units per CTA of the forward kernel
 constexpr int kMlpThreads = 256;
-constexpr int kHeadSplit = 8;    // CTAs per learner of the head kernel
+constexpr int kHeadSplit = 16;   // CTAs per learner of the head-gradient kernel
 
 __device__ __forceinline__ int batch_row(const int32_t* perm, int64_t pos0, int j, int b, int t) {
   return perm[pos0 + (int64_t)j * b + t];
@@ -85,9 +86,25 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_hidden_kernel(
     // for n <= 1024), and only then (rare; warp-uniform) is the dot redone
     // with the Dot2 accumulation.
     float sv = 0.f, sa = 0.f;
-    for (int f = lane; f < in_dim; f += 32) {
-      sv = __fmaf_rn(w[f], x[f], sv);
-      sa = __fmaf_rn(fabsf(w[f]), fabsf(x[f]), sa);
+    if ((in_dim & 3) == 0) {  // 128-bit shared-memory loads: half the instructions
+      const float4* w4 = reinterpret_cast<const float4*>(w);
+      const float4* x4 = reinterpret_cast<const float4*>(x);
+      for (int f = lane; f < (in_dim >> 2); f += 32) {
+        const float4 p = w4[f], q = x4[f];
+        sv = __fmaf_rn(p.x, q.x, sv);
+        sv = __fmaf_rn(p.y, q.y, sv);
+        sv = __fmaf_rn(p.z, q.z, sv);
+        sv = __fmaf_rn(p.w, q.w, sv);
+        sa = __fmaf_rn(fabsf(p.x), fabsf(q.x), sa);
+        sa = __fmaf_rn(fabsf(p.y), fabsf(q.y), sa);
+        sa = __fmaf_rn(fabsf(p.z), fabsf(q.z), sa);
+        sa = __fmaf_rn(fabsf(p.w), fabsf(q.w), sa);
+      }
+    } else {
+      for (int f = lane; f < in_dim; f += 32) {
+        sv = __fmaf_rn(w[f], x[f], sv);
+        sa = __fmaf_rn(fabsf(w[f]), fabsf(x[f]), sa);
+      }
     }
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) {
@@ -125,17 +142,58 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_hidden_kernel(
   }
 }
 
-__global__ void __launch_bounds__(kMlpThreads) mlp_head_kernel(
+// grid (r, b): the logits of one (learner, row) -- one warp per class over the
+// relu'd hidden row staged in shared memory -- and e = softmax - onehot(y)
+// (max-subtracted), written to E [r][b][classes].
+__global__ void __launch_bounds__(kMlpThreads) mlp_logits_kernel(
     const int32_t* __restrict__ y, const int32_t* __restrict__ perm, int64_t pos0, int b,
     int in_dim, int hidden, int classes, const float* __restrict__ Wall, int64_t ld, int j0,
-    const float2* __restrict__ A1, float* __restrict__ DA, float* __restrict__ Gall) {
+    const float2* __restrict__ A1, float* __restrict__ E) {
+  extern __shared__ __align__(16) float sm[];
+  float* hrow = sm;                 // [hidden]
+  __shared__ float lg[32];
+  const int slot = blockIdx.x, t = blockIdx.y;
+  const float* W2 = Wall + (int64_t)slot * ld + (int64_t)hidden * in_dim + hidden;
+  const float* b2 = W2 + (int64_t)classes * hidden;
+  const float2* a1 = A1 + ((int64_t)slot * b + t) * hidden;
+  for (int k = threadIdx.x; k < hidden; k += blockDim.x) {  // relu of the double-float a1
+    const float2 v = a1[k];
+    hrow[k] = (v.x > 0.f || (v.x == 0.f && v.y > 0.f)) ? __fadd_rn(v.x, v.y) : 0.f;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = warp; c < classes; c += nw) {
+    float s = 0.f;
+    for (int k = lane; k < hidden; k += 32) s = __fmaf_rn(__ldg(W2 + (int64_t)c * hidden + k), hrow[k], s);
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
+    if (lane == 0) lg[c] = __fadd_rn(s, b2[c]);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float mx = lg[0];
+    for (int c = 1; c < classes; ++c) mx = fmaxf(mx, lg[c]);
+    float den = 0.f;
+    for (int c = 0; c < classes; ++c) den = __fadd_rn(den, expf(__fsub_rn(lg[c], mx)));
+    const int yt = y[batch_row(perm, pos0, j0 + slot, b, t)];
+    float* e = E + ((int64_t)slot * b + t) * classes;
+    for (int c = 0; c < classes; ++c)
+      e[c] = __fsub_rn(__fdiv_rn(expf(__fsub_rn(lg[c], mx)), den), c == yt ? 1.f : 0.f);
+  }
+}
+
+// grid (r, kHeadSplit): slices of dW2 = e^T h / b, db2, and
+// da1 = (W2^T e) [a1 > 0] (written to DA for the dW1 kernel).
+__global__ void __launch_bounds__(kMlpThreads) mlp_head_kernel(
+    int b, int in_dim, int hidden, int classes, const float* __restrict__ Wall, int64_t ld,
+    const float2* __restrict__ A1, const float* __restrict__ E, float* __restrict__ DA,
+    float* __restrict__ Gall) {
   extern __shared__ __align__(16) float sm[];
   float* hs = sm;                              // [b][hidden]
   float* w2s = hs + b * hidden;                // [classes][hidden]
   float* e = w2s + classes * hidden;           // [b][classes]
   const int slot = blockIdx.x;
   const float* W2 = Wall + (int64_t)slot * ld + (int64_t)hidden * in_dim + hidden;
-  const float* b2 = W2 + (int64_t)classes * hidden;
   float* G = Gall + (int64_t)slot * ld;
   float* gW2 = G + (int64_t)hidden * in_dim + hidden;
   float* gb2 = gW2 + (int64_t)classes * hidden;
@@ -143,42 +201,17 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_head_kernel(
   __shared__ int zero_row;
   __shared__ __align__(8) uint64_t bar;
   if (threadIdx.x == 0) zero_row = 0;
+  for (int q = threadIdx.x; q < b * classes; q += blockDim.x) e[q] = E[(int64_t)slot * b * classes + q];
   __syncthreads();
   bulk::stage_rows_span(reinterpret_cast<float*>(a1),
                         reinterpret_cast<const float*>(A1 + (int64_t)slot * b * hidden), &zero_row,
                         1, 2 * b * hidden, 0, 0, w2s, W2, classes * hidden, &bar, 0, true);
-  // relu on the double-float pre-activation: positive iff hi > 0, or hi == 0 and lo > 0
   for (int q = threadIdx.x; q < b * hidden; q += blockDim.x) {
     const float2 v = a1[q];
     hs[q] = (v.x > 0.f || (v.x == 0.f && v.y > 0.f)) ? __fadd_rn(v.x, v.y) : 0.f;
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int pr = warp; pr < b * classes; pr += nw) {  // logits
-    const int t = pr / classes, c = pr - t * classes;
-    float s = 0.f;
-#pragma unroll 4
-    for (int k = lane; k < hidden; k += 32) s = __fmaf_rn(w2s[c * hidden + k], hs[t * hidden + k], s);
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
-    if (lane == 0) e[pr] = __fadd_rn(s, b2[c]);
-  }
-  __syncthreads();
-  if (threadIdx.x < b) {  // max-subtracted softmax, e = p - onehot(y)
-    const int t = threadIdx.x;
-    float mx = e[t * classes];
-    for (int c = 1; c < classes; ++c) mx = fmaxf(mx, e[t * classes + c]);
-    float den = 0.f;
-    for (int c = 0; c < classes; ++c) den = __fadd_rn(den, expf(__fsub_rn(e[t * classes + c], mx)));
-    const int yt = y[batch_row(perm, pos0, j0 + slot, b, t)];
-    for (int c = 0; c < classes; ++c)
-      e[t * classes + c] =
-          __fsub_rn(__fdiv_rn(expf(__fsub_rn(e[t * classes + c], mx)), den), c == yt ? 1.f : 0.f);
-  }
-  __syncthreads();
   const float fb = (float)b;
-  // every CTA of the learner recomputed the (cheap) logits; each writes its
-  // slice blockIdx.y of dW2 and of da1
   const int nsl = gridDim.y, sl = blockIdx.y;
   for (int q = sl * blockDim.x + threadIdx.x; q < classes * hidden; q += nsl * blockDim.x) {
     const int c = q / hidden, k = q - c * hidden;   // dW2 = e^T h / b
@@ -241,8 +274,11 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_w1_kernel(
 
 cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* perm, int64_t pos0,
                             int b, int in_dim, int hidden, int classes, const float* W, int64_t ld,
-                            int r, int j0, float2* A1, float* DA, float* G, cudaStream_t s) {
+                            int r, int j0, float2* A1, float* E, float* DA, float* G,
+                            cudaStream_t s) {
+  if (classes > 32) return cudaErrorInvalidValue;
   const size_t sm1 = sizeof(float) * ((size_t)b * in_dim + (size_t)kHidUnits * in_dim);
+  const size_t smL = sizeof(float) * (size_t)hidden;
   const size_t sm2 = sizeof(float) * ((size_t)b * hidden + (size_t)classes * hidden +
                                       (size_t)b * classes) +
                      16 + sizeof(float2) * (size_t)b * hidden;
@@ -254,14 +290,12 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
   if ((e = cudaFuncSetAttribute(mlp_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)sm2)) != cudaSuccess)
     return e;
-  if ((e = cudaFuncSetAttribute(mlp_w1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sm3)) != cudaSuccess)
-    return e;
-  const dim3 g1(r, (hidden + kHidUnits - 1) / kHidUnits), g2(r, kHeadSplit),
+  const dim3 g1(r, (hidden + kHidUnits - 1) / kHidUnits), gL(r, b), g2(r, kHeadSplit),
       g3(r, (hidden + kUnits - 1) / kUnits, (in_dim + kFeat - 1) / kFeat);
   mlp_hidden_kernel<<<g1, kMlpThreads, sm1, s>>>(X, perm, pos0, b, in_dim, hidden, W, ld, j0, A1);
-  mlp_head_kernel<<<g2, kMlpThreads, sm2, s>>>(y, perm, pos0, b, in_dim, hidden, classes, W, ld, j0,
-                                               A1, DA, G);
+  mlp_logits_kernel<<<gL, kMlpThreads, smL, s>>>(y, perm, pos0, b, in_dim, hidden, classes, W, ld,
+                                                 j0, A1, E);
+  mlp_head_kernel<<<g2, kMlpThreads, sm2, s>>>(b, in_dim, hidden, classes, W, ld, A1, E, DA, G);
   mlp_w1_kernel<<<g3, kMlpThreads, sm3, s>>>(X, perm, pos0, b, in_dim, hidden, j0, ld, DA, G);
   return cudaGetLastError();
 }

@@ -106,6 +106,7 @@ struct sma_handle {
   int kind = 0, in_dim = 0, hidden = 0, classes = 0, batch = 0;
   float2* mlp_A1 = nullptr;  // MLP scratch, sized for SMA_MAX_LOCAL_REPLICAS learners
   float* mlp_DA = nullptr;
+  float* mlp_E = nullptr;
   const float* X = nullptr;
   const int32_t* y = nullptr;
   int64_t n_samples = 0;
@@ -193,6 +194,7 @@ void free_all(sma_handle* h) {
   for (int i = 0; i < 2; ++i) cudaFree(h->perm_dev[i]);
   cudaFree(h->mlp_A1);
   cudaFree(h->mlp_DA);
+  cudaFree(h->mlp_E);
   if (h->perm_host) cudaFreeHost(h->perm_host);
   delete h;
 }
@@ -928,7 +930,12 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
     h->mlp_A1 = nullptr;
     h->mlp_DA = nullptr;
     const size_t n = (size_t)SMA_MAX_LOCAL_REPLICAS * batch * (kind == 1 ? hidden : classes);
-    if (kind == 1) CUDA_TRY(cudaMalloc(&h->mlp_A1, sizeof(float2) * n));
+    if (kind == 1) {
+      CUDA_TRY(cudaMalloc(&h->mlp_A1, sizeof(float2) * n));
+      cudaFree(h->mlp_E);
+      h->mlp_E = nullptr;
+      CUDA_TRY(cudaMalloc(&h->mlp_E, sizeof(float) * (size_t)SMA_MAX_LOCAL_REPLICAS * batch * classes));
+    }
     CUDA_TRY(cudaMalloc(&h->mlp_DA, sizeof(float) * n));
   }
   h->learner = true;
@@ -980,8 +987,9 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
     h->launches += 2;
   } else {
     CUDA_TRY(launch_mlp_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim, h->hidden,
-                             h->classes, h->W, h->d_pad, h->r, h->j0, h->mlp_A1, h->mlp_DA, h->G, s));
-    h->launches += 3;
+                             h->classes, h->W, h->d_pad, h->r, h->j0, h->mlp_A1, h->mlp_E,
+                             h->mlp_DA, h->G, s));
+    h->launches += 4;
   }
   for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
   return mark_done(h, s);
