@@ -23,6 +23,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/sma.h"
 #include "sma_host.h"
 #include "sma_internal.h"
@@ -36,6 +38,15 @@ using namespace sma;
       return fail(_e == cudaErrorMemoryAllocation ? SMA_ERR_OOM : SMA_ERR_CUDA,           \
                   "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
   } while (0)
+
+// NVTX ranges (header-only NVTX3: free unless a profiler such as nsys injects
+// itself) around the host-side enqueue of every phase of a round.
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 #define STATUS_TRY(expr)              \
   do {                                \
@@ -250,6 +261,7 @@ sma_status timer_pair(sma_handle* h, int phase, cudaEvent_t** out) {
 }
 
 sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s, int sms = 0) {
+  NvtxRange nvtx("sma.replica_kernel");
   if (sms <= 0) sms = h->num_sms;
   ReplicaArgs a{};
   a.W = h->W;
@@ -291,6 +303,7 @@ sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s, i
 // bracketed by timing events with SMA_FLAG_TIMING.
 sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float coef_b,
                          cudaStream_t s) {
+  NvtxRange nvtx(h->p2p ? "sma.zsync_p2p" : h->nvls ? "sma.zsync_nvls" : "sma.zsync_nccl");
   const size_t cnt = (size_t)h->shard_len;
   cudaEvent_t* tp = nullptr;
   if (h->p2p) {  // a6-a8 in one kernel over IPC-mapped peer memory
@@ -655,6 +668,7 @@ sma_status sma_synth_grads(sma_handle* h, int64_t round, uint64_t seed, void* st
 
 sma_status sma_step(sma_handle* h, void* stream) {
   if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  NvtxRange nvtx("sma_step");
   if (h->p2p && !h->p2p_connected)
     return fail(SMA_ERR_STATE, "SMA_FLAG_P2P_ZSYNC: call sma_p2p_connect on every rank first");
   for (int i = 0; i < h->r; ++i)
@@ -704,6 +718,7 @@ sma_status sma_step(sma_handle* h, void* stream) {
 
 sma_status sma_step_local(sma_handle* h, void* stream) {
   if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  NvtxRange nvtx("sma_step_local");
   for (int i = 0; i < h->r; ++i)
     if (!h->gptr[i])
       return fail(SMA_ERR_GRADS_MISSING, "learner %d has no registered gradient", h->j0 + i);
@@ -973,6 +988,7 @@ static sma_status learner_batch(sma_handle* h, int64_t round, cudaStream_t s, in
 
 sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
   if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  NvtxRange nvtx("sma_learner_grads");
   if (!h->learner) return fail(SMA_ERR_STATE, "no learner attached");
   if (round < 0) return fail(SMA_ERR_INVALID_ARG, "round < 0");
   if (h->r == 0) return SMA_OK;
@@ -997,6 +1013,7 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
 
 sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
   if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  NvtxRange nvtx("sma_learner_step");
   if (!h->learner) return fail(SMA_ERR_STATE, "no learner attached");
   if (round < 0) return fail(SMA_ERR_INVALID_ARG, "round < 0");
   const size_t fused_smem =
