@@ -68,6 +68,11 @@ def lib():
         L.orc_resize_replicas.restype = None
         L.orc_mlp_loss_grad.argtypes = [i32, i32, i32, i32, P, P, P, P, P, P]
         L.orc_mlp_loss_grad.restype = f64
+        L.orc_hier_round.argtypes = [i64, i32, i32, f64, f64, f64, f64, P, P, P, P, P, P]
+        L.orc_hier_round.restype = None
+        L.orc_hier_run_synth.argtypes = [i64, i32, i32, f64, f64, f64, f64, i64, u64, u64, i64,
+                                         P, P, P, P, P]
+        L.orc_hier_run_synth.restype = C.c_int
         _lib = L
     return _lib
 
@@ -248,3 +253,47 @@ def mlp_loss_grad(X, y, rows, params, in_dim=784, hidden=256, classes=10, want_g
 
 def mlp_dims(in_dim=784, hidden=256, classes=10) -> int:
     return hidden * in_dim + hidden + classes * hidden + classes
+
+
+# ------------------------------------------- NEXT-3: per-GPU reference models
+class HierState:
+    """fp64 state of the two-level rule of Section 3.3 (R20): replicas W [k][m],
+    reference models U [n][m] (row 0 mirrors z: GPU 0's reference model is the
+    central average model), z, z_prev."""
+
+    def __init__(self, W, U, z, z_prev):
+        self.W = _f64(W).copy()
+        self.U = _f64(U).copy()
+        self.z = _f64(z).copy()
+        self.z_prev = _f64(z_prev).copy()
+        self.U[0] = self.z
+
+    @classmethod
+    def init(cls, w0_vec, k: int, n: int, w_init=None, u_init=None):
+        w0_vec = _f64(w0_vec)
+        W = np.tile(w0_vec, (k, 1)) if w_init is None else _f64(w_init)
+        U = np.tile(w0_vec, (n, 1)) if u_init is None else _f64(u_init)
+        return cls(W, U, w0_vec, w0_vec)
+
+    def round(self, G, alpha_l, alpha_g, gamma, mu):
+        k, m = self.W.shape
+        n = self.U.shape[0]
+        G = _f64(G).reshape(k, m)
+        part = np.empty((n, m))
+        lib().orc_hier_round(m, n, k, alpha_l, alpha_g, gamma, mu, _p(self.W), _p(self.U),
+                             _p(self.z), _p(self.z_prev), _p(G), _p(part))
+        self.U[0] = self.z
+        return self
+
+
+def hier_run_synth(d, n, k, alpha_l, alpha_g, gamma, mu, R, seed_w, seed_g, idx=None):
+    """R rounds of the two-level rule (R20) on the synthetic inputs at indices
+    idx.  Returns (z, z_prev, W [k][m], U [n][m]; U[0] = z)."""
+    idx = _i64(np.arange(d) if idx is None else idx)
+    m = idx.size
+    z, zp, W, U = np.empty(m), np.empty(m), np.empty((k, m)), np.empty((n, m))
+    rc = lib().orc_hier_run_synth(d, n, k, alpha_l, alpha_g, gamma, mu, R, seed_w, seed_g, m,
+                                  _p(idx), _p(z), _p(zp), _p(W), _p(U))
+    if rc != 0:
+        raise MemoryError("oracle allocation failed")
+    return z, zp, W, U

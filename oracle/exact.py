@@ -50,3 +50,42 @@ def sma_exact(w0, grads, alpha, gamma, mu, w_init=None):
         z_prev = z_old                                            # line 14
         trace.append((list(z), list(z_prev), [list(r) for r in W]))
     return trace
+
+
+def hier_exact(w0, grads, n, alpha_l, alpha_g, gamma, mu, w_init=None, u_init=None):
+    """Exact two-level rule of Section 3.3 (reading R20):
+    per GPU g, d_j = alpha_l (w_j - u_g), w_j <- w_j - gamma G_j - d_j,
+    D_g = sum d_j; for g >= 1, c_g = alpha_g (u_g - z), u_g <- u_g + D_g - c_g;
+    z <- z + D_0 + sum_{g>=1} c_g + mu (z - z_prev), with u_0 = z and every
+    difference against the round-start values.  Learners are block-split over
+    the n GPUs (GPU g holds j with floor(g k/n) <= j < floor((g+1) k/n)).
+    Returns per-round (z, z_prev, W, U) with U[0] = z, initial state first."""
+    alpha_l, alpha_g = _frac(alpha_l), _frac(alpha_g)
+    gamma, mu = _frac(gamma), _frac(mu)
+    d = len(w0)
+    k = len(grads[0]) if grads else len(w_init)
+    gpu = [next(g for g in range(n) if g * k // n <= j < (g + 1) * k // n) for j in range(k)]
+    z = [_frac(v) for v in w0]
+    z_prev = list(z)
+    W = [list(z) for _ in range(k)] if w_init is None else [[_frac(v) for v in r] for r in w_init]
+    U = [list(z) for _ in range(n)] if u_init is None else [[_frac(v) for v in r] for r in u_init]
+    U[0] = list(z)
+    trace = [(list(z), list(z_prev), [list(r) for r in W], [list(r) for r in U])]
+    for g_round in grads:
+        ref = [list(z)] + [list(U[g]) for g in range(1, n)]     # round-start snapshots
+        D = [[Fraction(0)] * d for _ in range(n)]
+        for j in range(k):
+            g = gpu[j]
+            dj = [alpha_l * (W[j][p] - ref[g][p]) for p in range(d)]
+            W[j] = [W[j][p] - gamma * _frac(g_round[j][p]) - dj[p] for p in range(d)]
+            D[g] = [D[g][p] + dj[p] for p in range(d)]
+        c = [None] + [[alpha_g * (ref[g][p] - z[p]) for p in range(d)] for g in range(1, n)]
+        for g in range(1, n):
+            U[g] = [U[g][p] + D[g][p] - c[g][p] for p in range(d)]
+        z_old = list(z)
+        z = [z[p] + D[0][p] + sum((c[g][p] for g in range(1, n)), Fraction(0))
+             + mu * (z[p] - z_prev[p]) for p in range(d)]
+        z_prev = z_old
+        U[0] = list(z)
+        trace.append((list(z), list(z_prev), [list(r) for r in W], [list(r) for r in U]))
+    return trace

@@ -390,3 +390,101 @@ double orc_mlp_loss_grad(int32_t in_dim, int32_t hidden, int32_t classes, int32_
     free(a1); free(h); free(logit); free(e);
     return loss / (double)b;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-3: training multiple learners per GPU with per-GPU reference models  */
+/* (Section 3.3, fig:multiple_learners PAPER.md:656-662;   */
+/* formalised in SPEC.md S:327-335).  Reading R20:         */
+/*   * GPU g (n GPUs, learners block-split as orc_replica_location) has a    */
+/*     reference model u_g; GPU 0's reference model IS the central average   */
+/*     model z ("It uses one of the local reference models as the central    */
+/*     average model").  U[g] holds u_g for g >= 1; U[0]   */
+/*     is not used.                                                          */
+/*   * intra-GPU level ("each learner then computes the difference between   */
+/*     its model replica and the local reference model. This difference is   */
+/*     then applied to the respective replica"):    */
+/*        d_j = alpha_l (w_j - u_g);  w_j <- w_j - gamma G_j - d_j;          */
+/*        the reference model accumulates D_g = sum_{j on g} d_j.           */
+/*   * inter-GPU level ("the SMA algorithm is executed ... all other         */
+/*     reference models are the replicas"): Alg. 1 lines  */
+/*     9-14 over the replicas u_1..u_{n-1} (no gradient of their own):      */
+/*        c_g = alpha_g (u_g - z);  u_g <- u_g + D_g - c_g   (g >= 1)        */
+/*        z   <- z + D_0 + sum_{g>=1} c_g + mu (z - z_prev);  z_prev <- old z */
+/*   * every difference of a round is taken against the round-start values  */
+/*     (the snapshot rule of Alg. 1 line 9, applied at both levels), and the */
+/*     momentum term is Alg. 1's mu (z - z_prev) on round-start z / z_prev. */
+/*     With n = 1 this is exactly Alg. 1 with alpha = alpha_l.       */
+/* Sums in ascending local j, then ascending g.                              */
+/*   W [k][m], U [n][m] (row 0 unused), z, zprev [m], G [k][m] raw gradients,*/
+/*   part [n][m] scratch (part[g] = D_0 for g = 0, c_g for g >= 1).          */
+/* ------------------------------------------------------------------------ */
+void orc_hier_round(int64_t m, int32_t n, int32_t k, double alpha_l, double alpha_g,
+                    double gamma, double mu, double *W, double *U, double *z, double *zprev,
+                    const double *G, double *part) {
+    for (int32_t g = 0; g < n; g++) {
+        double *pg = part + (int64_t)g * m;
+        const double *ref = (g == 0) ? z : U + (int64_t)g * m;  /* u_0 = z */
+        for (int64_t p = 0; p < m; p++) pg[p] = 0.0;             /* D_g */
+        for (int32_t j = 0; j < k; j++) {
+            int32_t rank = -1, slot = -1;
+            orc_replica_location(k, n, j, &rank, &slot);
+            if (rank != g) continue;                             /* learners of GPU g */
+            double *w = W + (int64_t)j * m;
+            const double *Gj = G + (int64_t)j * m;
+            for (int64_t p = 0; p < m; p++) {
+                double gj = gamma * Gj[p];                       /* Alg. 1 line 8 */
+                double dj = alpha_l * (w[p] - ref[p]);           /* difference to u_g */
+                w[p] = w[p] - gj - dj;                           /* applied to the replica */
+                pg[p] = pg[p] + dj;                              /* D_g, ascending j */
+            }
+        }
+        if (g >= 1) {
+            double *u = U + (int64_t)g * m;
+            for (int64_t p = 0; p < m; p++) {
+                double D = pg[p];
+                double c = alpha_g * (u[p] - z[p]);              /* Alg. 1 line 9 over u_g */
+                u[p] = u[p] + D - c;                             /* absorbs D_g; line 10, no gradient */
+                pg[p] = c;
+            }
+        }
+    }
+    for (int64_t p = 0; p < m; p++) {
+        double s = 0.0;
+        for (int32_t g = 0; g < n; g++) s = s + part[(int64_t)g * m + p];  /* ascending g */
+        double zold = z[p];                                               /* line 11 */
+        z[p] = z[p] + s + mu * (z[p] - zprev[p]);                         /* line 13 */
+        zprev[p] = zold;                                                  /* line 14 */
+    }
+}
+
+/* R rounds of the two-level rule on the synthetic inputs at indices idx
+ * (separable per index, as orc_sma_run_synth).  Init: z = z_prev = w0 (R2),
+ * w_j = w0 (R3), u_g = w0 (every reference model starts as the initial
+ * model, like the average model it stands for).
+ * Outputs z, zprev [n_idx], and optionally W [k][n_idx], U [n][n_idx]. */
+int orc_hier_run_synth(int64_t d, int32_t n, int32_t k, double alpha_l, double alpha_g,
+                       double gamma, double mu, int64_t R, uint64_t seed_w, uint64_t seed_g,
+                       int64_t n_idx, const int64_t *idx, double *z_out, double *zprev_out,
+                       double *W_out, double *U_out) {
+    double *W = (double *)malloc(sizeof(double) * (size_t)k * (size_t)n_idx);
+    double *U = (double *)malloc(sizeof(double) * (size_t)n * (size_t)n_idx);
+    double *G = (double *)malloc(sizeof(double) * (size_t)k * (size_t)n_idx);
+    double *part = (double *)malloc(sizeof(double) * (size_t)n * (size_t)n_idx);
+    if (!W || !U || !G || !part) { free(W); free(U); free(G); free(part); return -1; }
+    orc_w0(n_idx, idx, seed_w, z_out);
+    for (int64_t t = 0; t < n_idx; t++) zprev_out[t] = z_out[t];
+    for (int32_t j = 0; j < k; j++) memcpy(W + (int64_t)j * n_idx, z_out, sizeof(double) * (size_t)n_idx);
+    for (int32_t g = 0; g < n; g++) memcpy(U + (int64_t)g * n_idx, z_out, sizeof(double) * (size_t)n_idx);
+    for (int64_t i = 0; i < R; i++) {
+        for (int32_t j = 0; j < k; j++)
+            orc_synth_grad(d, k, i, j, seed_g, n_idx, idx, G + (int64_t)j * n_idx);
+        orc_hier_round(n_idx, n, k, alpha_l, alpha_g, gamma, mu, W, U, z_out, zprev_out, G, part);
+    }
+    if (W_out) memcpy(W_out, W, sizeof(double) * (size_t)k * (size_t)n_idx);
+    if (U_out) {
+        memcpy(U_out, U, sizeof(double) * (size_t)n * (size_t)n_idx);
+        memcpy(U_out, z_out, sizeof(double) * (size_t)n_idx);   /* row 0: u_0 = z */
+    }
+    free(W); free(U); free(G); free(part);
+    return 0;
+}
