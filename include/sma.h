@@ -111,7 +111,20 @@ enum {
      * caller all-gathers the handles and every rank calls sma_p2p_connect()
      * before its first sma_step.  Several ranks may share one GPU.
      * Collective path only; exclusive with SMA_FLAG_NVLS_ZSYNC. */
-    SMA_FLAG_P2P_ZSYNC = 512u
+    SMA_FLAG_P2P_ZSYNC = 512u,
+    /* NEXT-3: "training multiple learners per GPU" with per-GPU reference
+     * models (Section 3.3; reading R20 in DESIGN.md).  GPU g keeps
+     * a reference model u_g; GPU 0's reference model is z.  Per
+     * round, against round-start values:
+     *   d_j = alpha (w_j - u_g);  w_j <- w_j - gamma g_j - d_j
+     *   c_g = alpha_g (u_g - z);  u_g <- u_g + sum_{j on g} d_j - c_g  (g >= 1)
+     *   z <- z + sum_{j on 0} d_j + sum_{g>=1} c_g + mu (z - z_prev)
+     * sma_config.alpha is the intra-GPU alpha_l; alpha_g is set with
+     * sma_set_alpha_global (default 1/(2(world-1))).  With one GPU this is
+     * exactly the flat Alg. 1.  Every z-sync variant (NCCL, P2P, NVLS, Mode A/B)
+     * carries it unchanged: only the per-GPU partial differs.  Not combined
+     * with SMA_FLAG_MATERIALIZE_C or SMA_FLAG_KERNEL_TMA. */
+    SMA_FLAG_HIERARCHICAL = 1024u
 };
 
 typedef struct {
@@ -246,12 +259,26 @@ sma_status sma_replica_device_ptr(sma_handle* h, int32_t j, const float** w_dev)
 sma_status sma_central_device_ptr(sma_handle* h, const float** z_dev);
 
 /* SMA restart: every local replica := z and
- * z_prev := z (zero momentum).  Enqueued on cuda_stream. */
+ * z_prev := z (zero momentum); with SMA_FLAG_HIERARCHICAL also u_g := z.
+ * Enqueued on cuda_stream. */
 sma_status sma_restart(sma_handle* h, void* cuda_stream);
 
 /* Change alpha, gamma, mu between rounds (online adaptation).
  * Errors: INVALID_ARG (non-finite). */
 sma_status sma_set_hparams(sma_handle* h, float alpha, float gamma, float mu);
+
+/* SMA_FLAG_HIERARCHICAL: set the inter-GPU correction weight alpha_g between
+ * rounds (every rank, same value).  Errors: STATE (not hierarchical),
+ * INVALID_ARG (non-finite). */
+sma_status sma_set_alpha_global(sma_handle* h, float alpha_g);
+
+/* SMA_FLAG_HIERARCHICAL: copy this rank's reference model u_g (d floats; on
+ * rank 0 -- and on a single-GPU handle -- that is z) into out / overwrite it
+ * from u (ranks >= 1 only: rank 0's reference model is set with
+ * sma_set_central).  Checkpoint/restore of the two-level state.  Synchronise.
+ * Errors: STATE (not hierarchical; set on rank 0), INVALID_ARG, CUDA. */
+sma_status sma_get_reference(sma_handle* h, float* out, int out_is_device);
+sma_status sma_set_reference(sma_handle* h, const float* u, int in_is_device);
 
 /* If SMA_FLAG_CHECK_FINITE: synchronise and report whether any non-finite
  * value has been produced so far (*flag = 1) ; clears the flag. */

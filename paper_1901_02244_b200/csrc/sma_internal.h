@@ -24,6 +24,14 @@ enum ReplicaMode : int {
   kPartialA = 1, // collective path, paper order: P = sum_{local j} c_j
   kPartialB = 2, // collective path, lookahead: Q = sum_{local j} (w_j' - z)
   kLocal = 3,    // local-only iteration (sync period tau > 1): w_j' = w_j - gamma g_j
+  // Two-level rule of Section 3.3 (SMA_FLAG_HIERARCHICAL, reading R20), GPU g >= 1
+  // with reference model u = U: d_j = alpha (w_j - u), D = sum d_j,
+  // c = alpha_g (u - z), u' = (u + D) - c, and out = c (Mode A) ...
+  kHierA = 4,
+  // ... or out = alpha_g (u' - z) (Mode B lookahead).
+  kHierB = 5,
+  // GPU 0 under Mode B: as kPartialB, but out = alpha * sum_j (w_j' - z).
+  kHierB0 = 6,
 };
 
 struct ReplicaArgs {
@@ -40,6 +48,8 @@ struct ReplicaArgs {
   float alpha, gamma, mu;
   int* nonfinite;      // CHECK_FINITE flag or nullptr
   int64_t c0;          // first float4 chunk this launch covers (LDG tail after TMA)
+  float* U;            // kHierA/B: this GPU's reference model u_g, updated in place [d_pad]
+  float alpha_g;       // kHierA/B: inter-GPU correction weight
 };
 
 // Launchers (return the launch error, never synchronise).
@@ -59,9 +69,11 @@ cudaError_t launch_reduce_corrections(int mode, const ReplicaArgs& a, int num_sm
 cudaError_t launch_zsync(int mode, const float* S, const float* z, float* zprev_next,
                          int64_t n4, float alpha, float mu, float coef_b, int* nonfinite,
                          int num_sms, cudaStream_t s);
-// Mode B prologue: Q = sum_j (w_j - zprev) over local replicas.
+// Mode B prologue: Q = scale * sum_j (w_j - zprev) over local replicas, or
+// Q = scale * (U - zprev) when U != nullptr (hierarchical, GPU g >= 1).
 cudaError_t launch_q_prologue(const float* W, int64_t ld, int r, const float* zprev, float* Q,
-                              int64_t n4, int num_sms, cudaStream_t s);
+                              int64_t n4, const float* U, float scale, int num_sms,
+                              cudaStream_t s);
 // Synthetic raw gradients of round `round` for local replicas [j0, j0 + r).
 cudaError_t launch_synth_grads(float* G, int64_t ld, int r, int j0, int k, int64_t d,
                                int64_t round, uint64_t seed, int num_sms, cudaStream_t s);

@@ -121,7 +121,7 @@ __device__ __forceinline__ void replica_update4(float4& w, const float4 g, const
   o = sma_elem(w.y, g.y, z.y, alpha, gamma); w.y = o.wn; c4.y = o.c;
   o = sma_elem(w.z, g.z, z.z, alpha, gamma); w.z = o.wn; c4.z = o.c;
   o = sma_elem(w.w, g.w, z.w, alpha, gamma); w.w = o.wn; c4.w = o.c;
-  if (MODE == kPartialB) {  // Q accumulates (w' - z), DESIGN.md "Mode B"
+  if (MODE == kPartialB || MODE == kHierB0) {  // Q accumulates (w' - z), DESIGN.md "Mode B"
     acc.x = __fadd_rn(acc.x, __fsub_rn(w.x, z.x));
     acc.y = __fadd_rn(acc.y, __fsub_rn(w.y, z.y));
     acc.z = __fadd_rn(acc.z, __fsub_rn(w.z, z.z));
@@ -145,10 +145,48 @@ constexpr int kThreads = 256;
 
 // Finish one float4 column chunk: the fused central update (n == 1) or the
 // per-GPU partial (collective path).
+// Reference model of the per-replica correction: z, or this GPU's u_g under
+// the two-level rule (kHierA/B), which the same thread also rewrites.
+template <int MODE>
+__device__ __forceinline__ float4 ld_ref(const ReplicaArgs& a, int64_t p0) {
+  if (MODE == kLocal) return make_float4(0.f, 0.f, 0.f, 0.f);
+  if (MODE == kHierA || MODE == kHierB) return ld_rw(a.U + p0);
+  return ld_ro(a.z + p0);
+}
+
+// Section 3.3 / R20 on one component: c = alpha_g (u - z); u' = (u + D) - c.
+__device__ __forceinline__ float hier_ref_elem(float u, float D, float zc, float ag, float& c) {
+  c = __fmul_rn(ag, __fsub_rn(u, zc));
+  return __fsub_rn(__fadd_rn(u, D), c);
+}
+
 template <int MODE>
 __device__ __forceinline__ void replica_finish(const ReplicaArgs& a, int64_t p0, const float4 z,
                                                const float4 acc, bool& bad) {
   if (MODE == kLocal) return;
+  if (MODE == kHierA || MODE == kHierB) {  // z holds u_g here (ld_ref)
+    const float4 zc = ld_ro(a.z + p0);
+    float4 un, c;
+    un.x = hier_ref_elem(z.x, acc.x, zc.x, a.alpha_g, c.x);
+    un.y = hier_ref_elem(z.y, acc.y, zc.y, a.alpha_g, c.y);
+    un.z = hier_ref_elem(z.z, acc.z, zc.z, a.alpha_g, c.z);
+    un.w = hier_ref_elem(z.w, acc.w, zc.w, a.alpha_g, c.w);
+    st4(a.U + p0, un);
+    if (MODE == kHierB) {  // lookahead partial alpha_g (u' - z^i)
+      c.x = __fmul_rn(a.alpha_g, __fsub_rn(un.x, zc.x));
+      c.y = __fmul_rn(a.alpha_g, __fsub_rn(un.y, zc.y));
+      c.z = __fmul_rn(a.alpha_g, __fsub_rn(un.z, zc.z));
+      c.w = __fmul_rn(a.alpha_g, __fsub_rn(un.w, zc.w));
+    }
+    st4(a.out + p0, c);
+    bad |= !finite4(un);
+    return;
+  }
+  if (MODE == kHierB0) {
+    st4(a.out + p0, make_float4(__fmul_rn(a.alpha, acc.x), __fmul_rn(a.alpha, acc.y),
+                                __fmul_rn(a.alpha, acc.z), __fmul_rn(a.alpha, acc.w)));
+    return;
+  }
   if (MODE == kFused) {
     const float4 zp = ld_rw(a.zprev_next + p0);
     float4 zn;
@@ -171,7 +209,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) replica_step_ldg(const R
   bool bad = false;
   for (int64_t c = a.c0 + (int64_t)blockIdx.x * kThreads + threadIdx.x; c < dfull4; c += stride) {
     const int64_t p0 = c << 2;
-    const float4 z = MODE == kLocal ? make_float4(0.f, 0.f, 0.f, 0.f) : ld_ro(a.z + p0);
+    const float4 z = ld_ref<MODE>(a, p0);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 c4;
     int j = 0;
@@ -204,7 +242,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) replica_step_ldg(const R
   const int64_t tail0 = dfull4 > a.c0 ? dfull4 : a.c0;
   for (int64_t c = tail0 + (int64_t)blockIdx.x * kThreads + threadIdx.x; c < a.n4; c += stride) {
     const int64_t p0 = c << 2;
-    const float4 z = MODE == kLocal ? make_float4(0.f, 0.f, 0.f, 0.f) : ld_ro(a.z + p0);
+    const float4 z = ld_ref<MODE>(a, p0);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     float4 c4;
     for (int j = 0; j < a.r; ++j) {
@@ -238,7 +276,7 @@ __global__ void __launch_bounds__(kThreads) replica_step_split(const ReplicaArgs
   const bool full = c < (a.d >> 2);
   const bool matc = a.C != nullptr;
   const int64_t p0 = c << 2;
-  const float4 z = valid ? ld_ro(a.z + p0) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 z = valid ? ld_ref<MODE>(a, p0) : make_float4(0.f, 0.f, 0.f, 0.f);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   float4 c4;
   bool bad = false;
@@ -387,23 +425,34 @@ __global__ void __launch_bounds__(kThreads) zsync_kernel(const float* __restrict
 }
 
 // Q = sum_j (w_j - z_prev) (Mode B prologue).
+// Hierarchical (R20): Q = scale (sum_j (w_j - z_prev)) on GPU 0 (scale = alpha_l),
+// Q = scale (u_g - z_prev) on GPU g >= 1 (U != nullptr, scale = alpha_g).
 __global__ void __launch_bounds__(kThreads) q_prologue_kernel(const float* __restrict__ W,
                                                               int64_t ld, int r,
                                                               const float* __restrict__ zp,
-                                                              float* __restrict__ Q, int64_t n4) {
+                                                              float* __restrict__ Q, int64_t n4,
+                                                              const float* __restrict__ U,
+                                                              float scale) {
   for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < n4;
        c += (int64_t)gridDim.x * kThreads) {
     const int64_t p0 = c << 2;
     const float4 z = ld_ro(zp + p0);
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j = 0; j < r; ++j) {
-      const float4 w = ld_ro(W + (int64_t)j * ld + p0);
-      acc.x = __fadd_rn(acc.x, __fsub_rn(w.x, z.x));
-      acc.y = __fadd_rn(acc.y, __fsub_rn(w.y, z.y));
-      acc.z = __fadd_rn(acc.z, __fsub_rn(w.z, z.z));
-      acc.w = __fadd_rn(acc.w, __fsub_rn(w.w, z.w));
+    if (U) {
+      const float4 u = ld_ro(U + p0);
+      acc = make_float4(__fsub_rn(u.x, z.x), __fsub_rn(u.y, z.y), __fsub_rn(u.z, z.z),
+                        __fsub_rn(u.w, z.w));
+    } else {
+      for (int j = 0; j < r; ++j) {
+        const float4 w = ld_ro(W + (int64_t)j * ld + p0);
+        acc.x = __fadd_rn(acc.x, __fsub_rn(w.x, z.x));
+        acc.y = __fadd_rn(acc.y, __fsub_rn(w.y, z.y));
+        acc.z = __fadd_rn(acc.z, __fsub_rn(w.z, z.z));
+        acc.w = __fadd_rn(acc.w, __fsub_rn(w.w, z.w));
+      }
     }
-    st4(Q + p0, acc);
+    st4(Q + p0, make_float4(__fmul_rn(scale, acc.x), __fmul_rn(scale, acc.y),
+                            __fmul_rn(scale, acc.z), __fmul_rn(scale, acc.w)));
   }
 }
 
@@ -680,6 +729,13 @@ cudaError_t launch_ldg_uj(const ReplicaArgs& a, int64_t work, int num_sms, cudaS
 }
 
 template <int MODE>
+cudaError_t launch_ldg_default(const ReplicaArgs& a, int64_t work, cudaStream_t s) {
+  const int grid = (int)((work + kThreads - 1) / kThreads);
+  replica_step_ldg<MODE, 2><<<grid < 1 ? 1 : grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int MODE>
 cudaError_t launch_ldg(const ReplicaArgs& a, int64_t work, int num_sms, cudaStream_t s) {
   switch (ldg_unroll()) {
     case 2: return launch_ldg_uj<MODE, 2>(a, work, num_sms, s);
@@ -695,7 +751,7 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
                                 cudaStream_t s) {
   ReplicaArgs a = a0;
   a.c0 = 0;
-  if (tma && mode != kLocal) {  // TMA-staged full tiles, then the LDG kernel for the rest
+  if (tma && (mode == kFused || mode == kPartialA || mode == kPartialB)) {  // TMA-staged full tiles, then the LDG kernel for the rest
     const int64_t nt = tma_full_tiles(a.d);
     cudaError_t e = launch_replica_step_tma(mode, a, nt, num_sms, s);
     if (e != cudaSuccess) return e;
@@ -724,6 +780,9 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
       case kFused: SMA_SPLIT_LAUNCH(kFused) break;
       case kPartialA: SMA_SPLIT_LAUNCH(kPartialA) break;
       case kPartialB: SMA_SPLIT_LAUNCH(kPartialB) break;
+      case kHierA: SMA_SPLIT_LAUNCH(kHierA) break;
+      case kHierB: SMA_SPLIT_LAUNCH(kHierB) break;
+      case kHierB0: SMA_SPLIT_LAUNCH(kHierB0) break;
       default: return cudaErrorInvalidValue;
     }
 #undef SMA_SPLIT_LAUNCH
@@ -734,6 +793,10 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
     case kPartialA: return launch_ldg<kPartialA>(a, work, num_sms, s);
     case kPartialB: return launch_ldg<kPartialB>(a, work, num_sms, s);
     case kLocal: return launch_ldg<kLocal>(a, work, num_sms, s);
+    // two-level rule: the default geometry only (no experiment-knob variants)
+    case kHierA: return launch_ldg_default<kHierA>(a, work, s);
+    case kHierB: return launch_ldg_default<kHierB>(a, work, s);
+    case kHierB0: return launch_ldg_default<kHierB0>(a, work, s);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -776,9 +839,10 @@ cudaError_t launch_zsync(int mode, const float* S, const float* z, float* zprev_
 }
 
 cudaError_t launch_q_prologue(const float* W, int64_t ld, int r, const float* zprev, float* Q,
-                              int64_t n4, int num_sms, cudaStream_t s) {
+                              int64_t n4, const float* U, float scale, int num_sms,
+                              cudaStream_t s) {
   q_prologue_kernel<<<grid_for(q_prologue_kernel, kThreads, 0, n4, num_sms), kThreads, 0, s>>>(
-      W, ld, r, zprev, Q, n4);
+      W, ld, r, zprev, Q, n4, U, scale);
   return cudaGetLastError();
 }
 

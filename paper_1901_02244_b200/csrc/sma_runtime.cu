@@ -70,6 +70,12 @@ struct sma_handle {
   bool collective = false, overlap = false, matc = false, tma = false, timing = false,
        graphs = false, check = false;
   float alpha = 0, gamma = 0, mu = 0;
+  // Section 3.3 two-level rule (SMA_FLAG_HIERARCHICAL, R20): alpha is alpha_l;
+  // U is this GPU's reference model u_g (ranks >= 1 of the collective path; on
+  // rank 0 the reference model is z itself)
+  bool hier = false;
+  float alpha_g = 0;
+  float* U = nullptr;      // [d_pad]
 
   float* W = nullptr;      // [r][d_pad]
   float* zbuf = nullptr;   // [2][d_pad]
@@ -201,6 +207,7 @@ void free_all(sma_handle* h) {
   cudaFree(h->Q);
   cudaFree(h->C);
   cudaFree(h->G);
+  cudaFree(h->U);
   cudaFree(h->nonfinite);
   for (int i = 0; i < 2; ++i) cudaFree(h->perm_dev[i]);
   cudaFree(h->mlp_A1);
@@ -278,10 +285,13 @@ sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s, i
   a.gamma = h->gamma;
   a.mu = h->mu;
   a.nonfinite = h->check ? h->nonfinite : nullptr;
+  a.U = h->U;
+  a.alpha_g = h->alpha_g;
   cudaEvent_t* tp = nullptr;
   STATUS_TRY(timer_pair(h, SMA_PHASE_REPLICA, &tp));
   if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
-  if (h->r > 0) {
+  // a reference model u_g is updated even on a GPU without learners
+  if (h->r > 0 || mode == kHierA || mode == kHierB) {
     CUDA_TRY(launch_replica_step(mode, h->tma, a, sms, s));
     ++h->launches;
     if (h->matc) {
@@ -296,6 +306,18 @@ sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s, i
   }
   if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
   return SMA_OK;
+}
+
+// Mode B shard update z' = (z + alpha_s S) + coef_b (z - z_prev): flat Alg. 1
+// emits Q = sum_j (w_j' - z) unscaled (alpha_s = alpha, coef_b = mu - alpha k);
+// the two-level rule emits pre-scaled partials (alpha_s = 1; coef_b in mode_b_coef).
+float zsync_alpha(const sma_handle* h) { return h->hier ? 1.f : h->alpha; }
+float mode_b_coef(const sma_handle* h) {
+  if (!h->hier) return h->mu - h->alpha * (float)h->cfg.k;
+  int32_t f0 = 0, r0 = 0;
+  sma_plan_local_replicas(h->cfg.k, h->cfg.world, 0, &f0, &r0);
+  // z^{i+1} = z^i + sum_g E_g - (alpha_l r_0 + alpha_g (n-1)) delta + mu delta
+  return h->mu - (h->alpha * (float)r0 + h->alpha_g * (float)(h->cfg.world - 1));
 }
 
 // a6-a8 on stream s: reduce-scatter the per-GPU partial, update this GPU's
@@ -315,7 +337,7 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
     a.off_zprev = reinterpret_cast<const char*>(h->zprev()) - h->p2p_region;
     a.off4 = h->shard_off / 4;
     a.len4 = h->shard_len / 4;
-    a.alpha = h->alpha;
+    a.alpha = zsync_alpha(h);
     a.mu = h->mu;
     a.coef_b = coef_b;
     a.n = h->cfg.world;
@@ -338,7 +360,7 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
     a.zprev = h->zprev();
     a.off4 = h->shard_off / 4;
     a.len4 = h->shard_len / 4;
-    a.alpha = h->alpha;
+    a.alpha = zsync_alpha(h);
     a.mu = h->mu;
     a.coef_b = coef_b;
     a.flag_uc = reinterpret_cast<unsigned*>(h->nv.uc);
@@ -360,7 +382,7 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
   STATUS_TRY(timer_pair(h, SMA_PHASE_SHARD_UPDATE, &tp));
   if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
   CUDA_TRY(launch_zsync(mode, h->S, h->z() + h->shard_off, h->zprev() + h->shard_off,
-                        h->shard_len / 4, h->alpha, h->mu, coef_b,
+                        h->shard_len / 4, zsync_alpha(h), h->mu, coef_b,
                         h->check ? h->nonfinite : nullptr, h->num_sms, s));
   if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
   STATUS_TRY(timer_pair(h, SMA_PHASE_ALL_GATHER, &tp));
@@ -375,18 +397,19 @@ sma_status enqueue_round(sma_handle* h, cudaStream_t s) {
   if (!h->collective) {  // n == 1: a3-a7 fused in one kernel
     STATUS_TRY(replica_launch(h, kFused, nullptr, s));
   } else if (!h->overlap) {  // Mode A: paper order (fig:dependencies d/e)
-    STATUS_TRY(replica_launch(h, kPartialA, h->P, s));
+    STATUS_TRY(replica_launch(h, h->U ? kHierA : kPartialA, h->P, s));
     STATUS_TRY(enqueue_zsync(h, kPartialA, h->P, 0.f, s));
     h->launches += 1;  // zsync (NCCL's own kernels are not counted)
   } else {  // Mode B: z-sync(i) on sB  ||  replica kernel(i) on s
     float* Qcur = h->Q + (int64_t)h->qi * h->d_pad;
     float* Qnext = h->Q + (int64_t)(1 - h->qi) * h->d_pad;
-    const float coef_b = h->mu - h->alpha * (float)h->cfg.k;
+    const float coef_b = mode_b_coef(h);
+    const int rmode = !h->hier ? kPartialB : (h->U ? kHierB : kHierB0);
     CUDA_TRY(cudaEventRecord(h->evFork, s));
     CUDA_TRY(cudaStreamWaitEvent(h->sB, h->evFork, 0));
     STATUS_TRY(enqueue_zsync(h, kPartialB, Qcur, coef_b, h->sB));
     CUDA_TRY(cudaEventRecord(h->evJoin, h->sB));
-    STATUS_TRY(replica_launch(h, kPartialB, Qnext, s, h->num_sms - h->sync_sms));
+    STATUS_TRY(replica_launch(h, rmode, Qnext, s, h->num_sms - h->sync_sms));
     CUDA_TRY(cudaStreamWaitEvent(s, h->evJoin, 0));
     h->launches += 1;  // zsync
   }
@@ -464,6 +487,12 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
                 h->r, cfg->rank, SMA_MAX_LOCAL_REPLICAS);
   if (h->matc && h->overlap)
     return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_MATERIALIZE_C is not combined with SMA_FLAG_OVERLAP");
+  h->hier = (f & SMA_FLAG_HIERARCHICAL) != 0;
+  if (h->hier && (h->matc || h->tma))
+    return fail(SMA_ERR_INVALID_ARG,
+                "SMA_FLAG_HIERARCHICAL is not combined with SMA_FLAG_MATERIALIZE_C or SMA_FLAG_KERNEL_TMA");
+  // R20 default: z's total pull alpha_l r + alpha_g (n-1) = 1 at alpha_l = 1/(2r)
+  h->alpha_g = 1.f / (2.f * (float)(cfg->world > 1 ? cfg->world - 1 : 1));
 
   int ndev = 0;
   CUDA_TRY(cudaGetDeviceCount(&ndev));
@@ -573,6 +602,7 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
     STATUS_TRY(alloc_zero(&h->zbuf, 2 * dp));
   }
   if (h->matc) STATUS_TRY(alloc_zero(&h->C, dp * (h->r > 0 ? h->r : 1)));
+  if (h->hier && h->collective && cfg->rank > 0) STATUS_TRY(alloc_zero(&h->U, dp));
   CUDA_TRY(cudaMalloc(&h->nonfinite, sizeof(int)));
   CUDA_TRY(cudaMemset(h->nonfinite, 0, sizeof(int)));
 
@@ -580,6 +610,8 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
   CUDA_TRY(cudaMemcpy(h->zbuf, w0, sizeof(float) * cfg->d, cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(h->zbuf + dp, h->zbuf, sizeof(float) * dp, cudaMemcpyDeviceToDevice));
   if (h->r > 0) CUDA_TRY(launch_broadcast_rows(h->W, h->d_pad, h->r, h->zbuf, h->n4, h->num_sms, 0));
+  if (h->U)  // R20: every reference model starts as the initial model
+    CUDA_TRY(cudaMemcpy(h->U, h->zbuf, sizeof(float) * dp, cudaMemcpyDeviceToDevice));
   CUDA_TRY(cudaDeviceSynchronize());
 
   return SMA_OK;
@@ -677,8 +709,9 @@ sma_status sma_step(sma_handle* h, void* stream) {
   DeviceGuard guard(h->dev);
   cudaStream_t s = (cudaStream_t)stream;
   if (h->overlap && h->q_dirty) {
+    const float scale = !h->hier ? 1.f : (h->U ? h->alpha_g : h->alpha);
     CUDA_TRY(launch_q_prologue(h->W, h->d_pad, h->r, h->zprev(), h->Q + (int64_t)h->qi * h->d_pad,
-                               h->n4, h->num_sms, s));
+                               h->n4, h->U, scale, h->num_sms, s));
     ++h->launches;
     h->q_dirty = false;
   }
@@ -882,8 +915,40 @@ sma_status sma_restart(sma_handle* h, void* stream) {
     CUDA_TRY(launch_broadcast_rows(h->W, h->d_pad, h->r, h->z(), h->n4, h->num_sms, s));
     ++h->launches;
   }
+  if (h->U)  // R20: the reference models restart from z as well
+    CUDA_TRY(cudaMemcpyAsync(h->U, h->z(), sizeof(float) * h->d_pad, cudaMemcpyDeviceToDevice, s));
   h->q_dirty = true;
   return mark_done(h, s);
+}
+
+sma_status sma_set_alpha_global(sma_handle* h, float alpha_g) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (!h->hier) return fail(SMA_ERR_STATE, "not a SMA_FLAG_HIERARCHICAL handle");
+  if (!finite_f(alpha_g)) return fail(SMA_ERR_INVALID_ARG, "non-finite alpha_g");
+  h->alpha_g = alpha_g;
+  h->q_dirty = true;  // Mode B: the pre-scaled partials change with alpha_g
+  ++h->ver;
+  return SMA_OK;
+}
+
+sma_status sma_get_reference(sma_handle* h, float* out, int out_is_device) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (!h->hier) return fail(SMA_ERR_STATE, "not a SMA_FLAG_HIERARCHICAL handle");
+  return copy_out(h, h->U ? h->U : h->z(), out, out_is_device);
+}
+
+sma_status sma_set_reference(sma_handle* h, const float* u, int in_is_device) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (!h->hier) return fail(SMA_ERR_STATE, "not a SMA_FLAG_HIERARCHICAL handle");
+  if (!h->U)
+    return fail(SMA_ERR_STATE, "rank %d's reference model is z (use sma_set_central)", h->cfg.rank);
+  if (!u) return fail(SMA_ERR_INVALID_ARG, "NULL input");
+  DeviceGuard guard(h->dev);
+  STATUS_TRY(sync_handle(h));
+  STATUS_TRY(copy_in(h, h->U, u, in_is_device));
+  CUDA_TRY(cudaStreamSynchronize(h->sIO));
+  h->q_dirty = true;
+  return SMA_OK;
 }
 
 sma_status sma_set_hparams(sma_handle* h, float alpha, float gamma, float mu) {
@@ -893,6 +958,7 @@ sma_status sma_set_hparams(sma_handle* h, float alpha, float gamma, float mu) {
   h->alpha = alpha;
   h->gamma = gamma;
   h->mu = mu;
+  if (h->hier) h->q_dirty = true;  // Mode B partials are pre-scaled by alpha_l (R20)
   ++h->ver;
   return SMA_OK;
 }

@@ -26,6 +26,7 @@ FLAG_KERNEL_TMA = 64
 FLAG_KERNEL_LDG = 128
 FLAG_NVLS_ZSYNC = 256
 FLAG_P2P_ZSYNC = 512
+FLAG_HIERARCHICAL = 1024
 P2P_HANDLE_BYTES = 64
 MAX_LOCAL_REPLICAS = 64
 NCCL_ID_BYTES = 128
@@ -44,7 +45,8 @@ EXPORTS = ["sma_create", "sma_destroy", "sma_set_learner_grads", "sma_set_learne
            "sma_plan_batch_indices", "sma_nccl_unique_id", "sma_kernel_time",
            "sma_launch_count", "sma_info", "sma_last_error", "sma_abi_version",
            "sma_step_local", "sma_autotune_step", "sma_set_local_replicas", "sma_learner_step",
-           "sma_p2p_handle", "sma_p2p_connect"]
+           "sma_p2p_handle", "sma_p2p_connect", "sma_set_alpha_global", "sma_get_reference",
+           "sma_set_reference"]
 
 
 class SmaError(RuntimeError):
@@ -109,6 +111,9 @@ def load():
         "sma_learner_step": ([P, i64, P], st),
         "sma_p2p_handle": ([P, P], st),
         "sma_p2p_connect": ([P, P], st),
+        "sma_set_alpha_global": ([P, C.c_float], st),
+        "sma_get_reference": ([P, P, C.c_int], st),
+        "sma_set_reference": ([P, P, C.c_int], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -226,6 +231,18 @@ def sma_restart(h: int, stream=None) -> None:
 
 def sma_set_hparams(h: int, alpha: float, gamma: float, mu: float) -> None:
     _check(load().sma_set_hparams(h, alpha, gamma, mu), "sma_set_hparams")
+
+
+def sma_set_alpha_global(h: int, alpha_g: float) -> None:
+    _check(load().sma_set_alpha_global(h, alpha_g), "sma_set_alpha_global")
+
+
+def sma_get_reference(h: int, out, out_is_device: bool) -> None:
+    _check(load().sma_get_reference(h, _ptr(out), int(out_is_device)), "sma_get_reference")
+
+
+def sma_set_reference(h: int, u, in_is_device: bool) -> None:
+    _check(load().sma_set_reference(h, _ptr(u), int(in_is_device)), "sma_set_reference")
 
 
 def sma_check_finite(h: int) -> bool:
@@ -418,6 +435,18 @@ class Sma:
 
     def set_hparams(self, alpha, gamma, mu):
         sma_set_hparams(self.h, alpha, gamma, mu)
+
+    def set_alpha_global(self, alpha_g):
+        sma_set_alpha_global(self.h, alpha_g)
+
+    def reference(self) -> np.ndarray:
+        out = np.empty(self.d, np.float32)
+        sma_get_reference(self.h, out, False)
+        return out
+
+    def set_reference(self, u):
+        u = np.ascontiguousarray(u, np.float32)
+        sma_set_reference(self.h, u, False)
 
     def kernel_time(self, reset=False, phase=PHASE_REPLICA):
         return sma_kernel_time(self.h, phase, reset)

@@ -580,3 +580,60 @@ def test_randomized_configs(torch_cuda, S, orc):
         for j in range(k):
             assert relerr(h.replica(j), Wr[j]) <= TOL, ctx
         h.close()
+
+
+# ------------------------------ Section 3.3 two-level rule (R20), one GPU
+@pytest.mark.parametrize("variant", ["fused", "fused_graph", "collA", "collA_graph", "p2pA",
+                                     "collB", "collB_graph", "p2pB", "p2pB_graph"])
+def test_hierarchical_one_gpu_is_flat_sma(torch_cuda, S, variant):
+    """SMA_FLAG_HIERARCHICAL on one GPU: GPU 0's reference model is z, so the
+    two-level rule collapses to flat Alg. 1: bitwise equal to
+    the flat handle where the arithmetic is the same (fused, Mode A), within
+    the tolerance of the (pinned) two-level oracle everywhere (Mode B pre-scales
+    its partial), 40 rounds at a ragged size."""
+    d, k, R = 100_003, 4, 40
+    a, g, m = F32(1 / 8), F32(0.1), F32(0.9)
+    flags = COLLECTIVE_FLAGS[variant]
+    hh = run_synth_gpu(torch_cuda, S, d, k, R, a, g, m, flags | S.FLAG_HIERARCHICAL)
+    import oracle
+    zr, zpr, Wr, Ur = oracle.hier_run_synth(
+        d, 1, k, a, 0.5, g, m, R, sma_inputs.SEED_W, sma_inputs.SEED_G)
+    z = hh.central()
+    assert relerr(z, zr) <= TOL and relerr(hh.central_prev(), zpr) <= TOL
+    for j in range(k):
+        assert relerr(hh.replica(j), Wr[j]) <= TOL
+    assert np.array_equal(hh.reference(), z)          # u_0 = z
+    if not flags & S.FLAG_OVERLAP:
+        hf = run_synth_gpu(torch_cuda, S, d, k, R, a, g, m, flags)
+        assert np.array_equal(hf.central(), z)
+        for j in range(k):
+            assert np.array_equal(hf.replica(j), hh.replica(j))
+        hf.close()
+    hh.close()
+
+
+def test_hierarchical_api_states(torch_cuda, S):
+    """Reference-model calls on the wrong handle fail with SMA_ERR_STATE and
+    change nothing; restart also resets the reference model (u_0 = z)."""
+    d = 1000
+    flat = S.Sma(d, 2, 0.25, 0.1, 0.9, sma_inputs.w0(d))
+    for call in (lambda: flat.set_alpha_global(0.5), lambda: flat.reference()):
+        with pytest.raises(S.SmaError, match="SMA_ERR_STATE"):
+            call()
+    flat.close()
+    h = S.Sma(d, 2, 0.25, 0.1, 0.9, sma_inputs.w0(d), flags=S.FLAG_HIERARCHICAL)
+    with pytest.raises(S.SmaError, match="SMA_ERR_STATE"):
+        h.set_reference(np.zeros(d, np.float32))       # rank 0's reference model is z
+    with pytest.raises(S.SmaError, match="SMA_ERR_INVALID_ARG"):
+        h.set_alpha_global(float("nan"))
+    st = torch_cuda.cuda.current_stream()
+    for i in range(3):
+        h.synth_grads(i, sma_inputs.SEED_G, st)
+        h.step(st)
+    h.restart(st)
+    z = h.central()
+    assert np.array_equal(h.reference(), z) and np.array_equal(h.central_prev(), z)
+    for bad in (S.FLAG_MATERIALIZE_C, S.FLAG_KERNEL_TMA):
+        with pytest.raises(S.SmaError, match="SMA_ERR_INVALID_ARG"):
+            S.Sma(d, 2, 0.25, 0.1, 0.9, sma_inputs.w0(d), flags=S.FLAG_HIERARCHICAL | bad)
+    h.close()

@@ -13,6 +13,8 @@ import sys
 import numpy as np
 import pytest
 
+from oracle import exact
+
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -78,3 +80,106 @@ def test_p2p_ranks_on_one_gpu_match_oracle(orc, tmp_path, world, k, mode):
     assert rel(np.load(tmp_path / "zp0.npy"), zpr) <= 1e-5
     for j in range(k):
         assert rel(np.load(tmp_path / f"w{j}.npy"), Wr[j]) <= 1e-5
+
+
+# --------------------------------------- Section 3.3 two-level rule (R20)
+def _hier_worker(rank, world, port, flags, d, k, R, al, ag, dyadic, out):
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import sma_inputs
+    from paper_1901_02244_b200 import sma
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g, m = (0.125, 0.5) if dyadic else (float(np.float32(0.1)), float(np.float32(0.9)))
+    w0 = sma_inputs.dyadic(d, 300).astype(np.float32) if dyadic else sma_inputs.w0(d)
+    h = sma.Sma(d, k, al, g, m, w0, rank=rank, world=world, device=0,
+                flags=flags | sma.FLAG_P2P_ZSYNC | sma.FLAG_HIERARCHICAL)
+    if ag is not None:
+        h.set_alpha_global(ag)
+    handles = [None] * world
+    dist.all_gather_object(handles, sma.sma_p2p_handle(h.h))
+    sma.sma_p2p_connect(h.h, handles)
+    dist.barrier()
+    s = torch.cuda.Stream()
+    if dyadic:
+        G = torch.tensor(sma_inputs.dyadic((R, k, d), 301), dtype=torch.float32, device="cuda")
+    for i in range(R):
+        if dyadic:
+            for j in h.local_replicas():
+                h.set_grads(j, G[i, j])
+        else:
+            h.synth_grads(i, sma_inputs.SEED_G, s)
+        h.step(s)
+    s.synchronize()
+    np.save(os.path.join(out, f"z{rank}.npy"), h.central())
+    np.save(os.path.join(out, f"zp{rank}.npy"), h.central_prev())
+    np.save(os.path.join(out, f"u{rank}.npy"), h.reference())
+    for j in h.local_replicas():
+        np.save(os.path.join(out, f"w{j}.npy"), h.replica(j))
+    dist.barrier()
+    h.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,k,ag", [(2, 4, None), (3, 7, 0.25), (4, 8, None)])
+@pytest.mark.parametrize("mode", ["A", "B", "B_graph"])
+def test_p2p_hierarchical_ranks_match_oracle(orc, tmp_path, world, k, ag, mode):
+    """SMA_FLAG_HIERARCHICAL with 2-4 ranks (processes) on one GPU over the P2P
+    z-sync: z, z_prev, every replica and every GPU's reference model u_g match
+    the two-level fp64 oracle (R20) after 12 rounds; z is bitwise equal on
+    every rank; rank 0's reference model is z."""
+    import torch.multiprocessing as mp
+
+    import sma_inputs
+    flags = {"A": 0, "B": 1, "B_graph": 1 | 8}[mode]
+    d, R = 100_003, 12
+    al = float(np.float32(0.25))
+    ag_eff = float(np.float32(ag if ag is not None else 1 / (2 * (world - 1))))
+    mp.spawn(_hier_worker, args=(world, _port(), flags, d, k, R, al, ag, False, str(tmp_path)),
+             nprocs=world)
+    zr, zpr, Wr, Ur = orc.hier_run_synth(d, world, k, al, ag_eff, float(np.float32(0.1)),
+                                         float(np.float32(0.9)), R, sma_inputs.SEED_W,
+                                         sma_inputs.SEED_G)
+    zs = [np.load(tmp_path / f"z{g}.npy") for g in range(world)]
+    for z in zs[1:]:
+        assert np.array_equal(z, zs[0])
+    assert np.array_equal(np.load(tmp_path / "u0.npy"), zs[0])
+    rel = lambda x, y: np.max(np.abs(x - y) / (1 + np.abs(y)))  # noqa: E731
+    assert rel(zs[0], zr) <= 1e-5
+    assert rel(np.load(tmp_path / "zp0.npy"), zpr) <= 1e-5
+    for g in range(1, world):
+        assert rel(np.load(tmp_path / f"u{g}.npy"), Ur[g]) <= 1e-5, g
+    for j in range(k):
+        assert rel(np.load(tmp_path / f"w{j}.npy"), Wr[j]) <= 1e-5, j
+    # the two levels matter: the result is not flat Alg. 1
+    zf, _, _ = orc.run_synth(d, k, al, float(np.float32(0.1)), float(np.float32(0.9)), R,
+                             sma_inputs.SEED_W, sma_inputs.SEED_G)
+    assert rel(zs[0], zf) > 1e-4
+
+
+@pytest.mark.parametrize("world,k", [(2, 4), (3, 5)])
+@pytest.mark.parametrize("mode", ["A", "B"])
+def test_p2p_hierarchical_dyadic_bitwise(tmp_path, world, k, mode):
+    """Dyadic inputs keep fp32 exact for the first rounds: the multi-rank GPU
+    two-level rule equals the exact-rational brute force (oracle/exact.py)
+    bit for bit -- replicas, reference models, z and z_prev."""
+    import torch.multiprocessing as mp
+
+    import sma_inputs
+    d, R = 4, 6
+    al, ag = 0.25, 0.5
+    mp.spawn(_hier_worker, args=(world, _port(), {"A": 0, "B": 1}[mode], d, k, R, al, ag, True,
+                                 str(tmp_path)), nprocs=world)
+    w0 = sma_inputs.dyadic(d, 300)
+    G = sma_inputs.dyadic((R, k, d), 301)
+    z, zp, W, U = exact.hier_exact(list(w0), G.tolist(), world, al, ag, 0.125, 0.5)[R]
+    assert np.load(tmp_path / "z0.npy").tolist() == [float(v) for v in z]
+    assert np.load(tmp_path / "zp0.npy").tolist() == [float(v) for v in zp]
+    for g in range(world):
+        assert np.load(tmp_path / f"u{g}.npy").tolist() == [float(v) for v in U[g]], g
+    for j in range(k):
+        assert np.load(tmp_path / f"w{j}.npy").tolist() == [float(v) for v in W[j]], j
