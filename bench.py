@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--tau", type=int, default=1,
                     help="synchronise every tau iterations (sma_step_local on the others; "
                          "0 = never: the paper's 'no synchronisation' point, fig:overhead)")
+    ap.add_argument("--hier", action="store_true",
+                    help="Section 3.3 two-level rule (per-GPU reference models, R20): "
+                         "alpha_l = 1/(2r), alpha_g = 1/(2(N-1)); identical to flat SMA at N = 1")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -242,6 +245,9 @@ def main():
         flags |= sma.FLAG_NVLS_ZSYNC
     if args.zsync in ("p2p", "auto") and collective:
         flags |= sma.FLAG_P2P_ZSYNC
+    if args.hier:   # alpha is the intra-GPU alpha_l = 1/(2r); alpha_g keeps libsma's default
+        flags |= sma.FLAG_HIERARCHICAL
+        alpha = float(np.float32(1 / (2 * max(1, k // world))))
 
     nccl_id = nccl_id_a = None
     if world > 1:   # one NCCL id per libsma communicator (the bench may create two)
@@ -448,7 +454,7 @@ def main():
             "config": {"workload": workload_name(args.config, d, k), "d": d, "d_pad": d_pad,
                        "k": k, "replicas_per_gpu": r, "alpha": alpha, "gamma": gamma, "mu": mu,
                        "mode": mode, "kernel": kvar,
-                       "materialize_c": bool(args.matc),
+                       "materialize_c": bool(args.matc), "hierarchical": bool(args.hier),
                        "parallelism": f"sma-dp{world}" + ("" if not collective else
                                                            f"+{zsync}-zsync"),
                        "l2": "no flush: per-round working set "

@@ -42,6 +42,8 @@ def _worker(rank, world, port, flags, d, k, R, out):
     obj = [sma.sma_nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     a, g, m = (float(np.float32(x)) for x in (1 / k, 0.1, 0.9))
+    if flags & sma.FLAG_HIERARCHICAL:
+        a = float(np.float32(0.25))
     h = sma.Sma(d, k, a, g, m, sma_inputs.w0(d), rank=rank, world=world, device=rank,
                 nccl_id=obj[0], flags=flags)
     if flags & sma.FLAG_P2P_ZSYNC:
@@ -55,6 +57,8 @@ def _worker(rank, world, port, flags, d, k, R, out):
     np.save(os.path.join(out, f"z{rank}.npy"), h.central())
     for j in h.local_replicas():
         np.save(os.path.join(out, f"w{j}.npy"), h.replica(j))
+    if flags & sma.FLAG_HIERARCHICAL:
+        np.save(os.path.join(out, f"u{rank}.npy"), h.reference())
     h.close()
     dist.barrier()
     dist.destroy_process_group()
@@ -83,3 +87,27 @@ def test_multi_gpu_matches_oracle(orc, tmp_path, flags):
     for j in range(k):
         w = np.load(tmp_path / f"w{j}.npy")
         assert np.max(np.abs(w - Wr[j]) / (1 + np.abs(Wr[j]))) <= 1e-5
+
+
+@pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("flags", [1024, 1024 | 1, 1024 | 1 | 8, 1024 | 512, 1024 | 1 | 512])
+def test_multi_gpu_hierarchical_matches_oracle(orc, tmp_path, flags):
+    """Section 3.3 two-level rule (R20) on real GPUs (NCCL or P2P z-sync)."""
+    import torch.multiprocessing as mp
+
+    import sma_inputs
+    world = min(_ngpus(), 8)
+    d, k, R = 100_003, 2 * world, 50
+    mp.spawn(_worker, args=(world, _port(), flags, d, k, R, str(tmp_path)), nprocs=world)
+    f = lambda x: float(np.float32(x))  # noqa: E731
+    zr, _, Wr, Ur = orc.hier_run_synth(d, world, k, f(0.25), f(1 / (2 * (world - 1))), f(0.1),
+                                       f(0.9), R, sma_inputs.SEED_W, sma_inputs.SEED_G)
+    rel = lambda x, y: np.max(np.abs(x - y) / (1 + np.abs(y)))  # noqa: E731
+    zs = [np.load(tmp_path / f"z{g}.npy") for g in range(world)]
+    for z in zs[1:]:
+        assert np.array_equal(z, zs[0])
+    assert rel(zs[0], zr) <= 1e-5
+    for g in range(world):
+        assert rel(np.load(tmp_path / f"u{g}.npy"), Ur[g]) <= 1e-5
+    for j in range(k):
+        assert rel(np.load(tmp_path / f"w{j}.npy"), Wr[j]) <= 1e-5
