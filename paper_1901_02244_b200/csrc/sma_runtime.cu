@@ -20,6 +20,7 @@
 #include <unistd.h>
 
 #include <cmath>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -392,8 +393,14 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
   return SMA_OK;
 }
 
-// The body of one round, enqueued on stream s (capturable).
-sma_status enqueue_round(sma_handle* h, cudaStream_t s) {
+// The body of one round, enqueued on stream s (capturable without a learner).
+// `learner` (optional) enqueues this round's learner gradients (a2') on s
+// before the replica kernel; in Mode B it is enqueued AFTER the z-sync fork, so
+// the global synchronisation runs concurrently with the learning tasks -- the
+// paper's overlap of GlobalSync with Learning (fig:dependencies f).
+using LearnerFn = std::function<sma_status(cudaStream_t)>;
+sma_status enqueue_round(sma_handle* h, cudaStream_t s, const LearnerFn* learner = nullptr) {
+  if (learner && !(h->collective && h->overlap)) STATUS_TRY((*learner)(s));
   if (!h->collective) {  // n == 1: a3-a7 fused in one kernel
     STATUS_TRY(replica_launch(h, kFused, nullptr, s));
   } else if (!h->overlap) {  // Mode A: paper order (fig:dependencies d/e)
@@ -409,6 +416,7 @@ sma_status enqueue_round(sma_handle* h, cudaStream_t s) {
     CUDA_TRY(cudaStreamWaitEvent(h->sB, h->evFork, 0));
     STATUS_TRY(enqueue_zsync(h, kPartialB, Qcur, coef_b, h->sB));
     CUDA_TRY(cudaEventRecord(h->evJoin, h->sB));
+    if (learner) STATUS_TRY((*learner)(s));   // Learning(i) || GlobalSync(i)
     STATUS_TRY(replica_launch(h, rmode, Qnext, s, h->num_sms - h->sync_sms));
     CUDA_TRY(cudaStreamWaitEvent(s, h->evJoin, 0));
     h->launches += 1;  // zsync
@@ -1086,6 +1094,27 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
       (sizeof(float) * (32 + (size_t)h->classes) + sizeof(int)) * (size_t)h->r * h->batch;
   const bool fusable = h->kind == 0 && !h->collective && !h->matc && h->r > 0 &&
                        h->classes <= 16 && fused_smem <= 200 * 1024 && !h->graphs;
+  if (!fusable && h->collective && h->overlap && !h->graphs) {
+    // Mode B: the z-sync of this round is forked first and overlaps the
+    // learner kernels and the replica kernel
+    NvtxRange nvtx2("sma_learner_step.overlap");
+    if (h->p2p && !h->p2p_connected)
+      return fail(SMA_ERR_STATE, "SMA_FLAG_P2P_ZSYNC: call sma_p2p_connect on every rank first");
+    DeviceGuard guard(h->dev);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (h->q_dirty) {
+      const float scale = !h->hier ? 1.f : (h->U ? h->alpha_g : h->alpha);
+      CUDA_TRY(launch_q_prologue(h->W, h->d_pad, h->r, h->zprev(),
+                                 h->Q + (int64_t)h->qi * h->d_pad, h->n4, h->U, scale,
+                                 h->num_sms, s));
+      ++h->launches;
+      h->q_dirty = false;
+    }
+    const LearnerFn fn = [&](cudaStream_t ls) { return sma_learner_grads(h, round, ls); };
+    STATUS_TRY(enqueue_round(h, s, &fn));
+    advance(h);
+    return mark_done(h, s);
+  }
   if (!fusable) {  // the same result through the two public calls
     STATUS_TRY(sma_learner_grads(h, round, stream));
     return sma_step(h, stream);

@@ -637,3 +637,54 @@ def test_hierarchical_api_states(torch_cuda, S):
         with pytest.raises(S.SmaError, match="SMA_ERR_INVALID_ARG"):
             S.Sma(d, 2, 0.25, 0.1, 0.9, sma_inputs.w0(d), flags=S.FLAG_HIERARCHICAL | bad)
     h.close()
+
+
+@pytest.mark.parametrize("kind,variant", [(0, "collB"), (0, "p2pB"), (1, "collB"), (1, "p2pB")])
+def test_learner_step_overlapped_zsync(torch_cuda, S, orc, kind, variant):
+    """Mode B sma_learner_step forks the z-sync of round i before the learner
+    kernels of round i (GlobalSync || Learning, fig:dependencies f):
+    the same arithmetic as sma_learner_grads + sma_step, so bitwise equal to it
+    over 40 rounds crossing an epoch, and within tolerance of the oracle
+    (softmax: C1 shape; MLP: 784-256-10, margin-conditioned as R18)."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(3_000, seed=4 if kind == 0 else 13)
+    d = 7850 if kind == 0 else MLP_D
+    k, b, R = 4, 8, 40
+    a, g, m = F32(1 / k), F32(0.1 if kind == 0 else 0.05), F32(0.9)
+    w0 = np.zeros(d, np.float32) if kind == 0 else \
+        np.random.default_rng(6).normal(0, 0.05, d).astype(np.float32)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    hs = []
+    for overlapped in (True, False):
+        h = S.Sma(d, k, a, g, m, w0, flags=COLLECTIVE_FLAGS[variant])
+        S.sma_learner_attach(h.h, kind, 784, 256 if kind else 0, 10, b, Xd, yd, X.shape[0], 99)
+        s = torch.cuda.Stream()
+        for i in range(R):
+            if overlapped:
+                S.sma_learner_step(h.h, i, s)
+            else:
+                S.sma_learner_grads(h.h, i, s)
+                h.step(s)
+        hs.append(h)
+    assert np.array_equal(hs[0].central(), hs[1].central())
+    assert np.array_equal(hs[0].central_prev(), hs[1].central_prev())
+    for j in range(k):
+        assert np.array_equal(hs[0].replica(j), hs[1].replica(j))
+    if kind == 0:
+        zr, _, _ = orc.run_softmax(X, y, b, 99, k, a, g, m, R, w0.astype(np.float64))
+        assert relerr(hs[0].central(), zr) <= TOL
+    else:
+        st = orc.State.init(w0.astype(np.float64), k)
+        mm = np.inf
+        for i in range(R):
+            G = []
+            for j in range(k):
+                _, gj, mg = orc.mlp_loss_grad(X, y, orc.batch_indices(X.shape[0], k, b, 99, i, j),
+                                              st.W[j])
+                G.append(gj)
+                mm = min(mm, mg)
+            st.round(np.stack(G), a, g, m)
+        if mm > 5e-6:
+            assert relerr(hs[0].central(), st.z) <= TOL
+    for h in hs:
+        h.close()
