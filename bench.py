@@ -216,10 +216,21 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    # SMA_BENCH_SHARED_GPU=1 (testing only): every rank on cuda:0, gloo for the
+    # host-side plumbing and the P2P z-sync (NCCL cannot put two ranks on one
+    # GPU), so the N > 1 code path of this script runs on a 1-GPU box
+    shared = os.environ.get("SMA_BENCH_SHARED_GPU") == "1" and world > 1
+    if shared:
+        local = 0
+        args.zsync = "p2p"
     torch.cuda.set_device(local)
+    red_dev = "cpu" if shared else "cuda"   # device of the small reduction tensors
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     cfg = sma_inputs.CONFIGS[args.config]
     d = cfg["d"]
@@ -274,7 +285,7 @@ def main():
             h = make_handle(flags)
         except Exception as e:  # noqa: BLE001 -- any setup failure selects NCCL
             ok, err = 0, str(e)
-        flag_t = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        flag_t = torch.tensor([ok], dtype=torch.int32, device=red_dev)
         dist.all_reduce(flag_t, op=dist.ReduceOp.MIN)
         if int(flag_t[0]) == 0:
             if h is not None:
@@ -347,7 +358,7 @@ def main():
         pm, pn = h.kernel_time(reset=True, phase=ph)
         phase_avg.append(pm / pn if pn else 0.0)
 
-    t = torch.tensor([ms, *phase_avg, float(launches)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([ms, *phase_avg, float(launches)], dtype=torch.float64, device=red_dev)
     if world > 1:
         tmax = t.clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -386,7 +397,7 @@ def main():
         for ph in range(5):
             pm, pn = hA.kernel_time(reset=True, phase=ph)
             pa.append(pm / pn if pn else 0.0)
-        ta = torch.tensor([e0.elapsed_time(e1) / ns, *pa], dtype=torch.float64, device="cuda")
+        ta = torch.tensor([e0.elapsed_time(e1) / ns, *pa], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(ta, op=dist.ReduceOp.MAX)
         serial = [float(x) for x in ta]
@@ -412,7 +423,7 @@ def main():
         for _ in range(args.e2e_steps):
             e2e_step()
         barrier()
-        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
         e2e = {"value": args.e2e_steps / float(e2e_s[0]), "unit": UNIT,
@@ -431,6 +442,8 @@ def main():
         else:
             alg_bytes = 4 * d_pad * (3 * r + 2)
             kname = f"replica_step_{kvar}<kPartial{mode}>"
+            if args.hier and mode == "B":   # rank 0 emits the pre-scaled partial (R20)
+                kname = f"replica_step_{kvar}<kHierB0>"
         if args.matc:   # replica kernel: r x (read w, g; write w, c) + z; reduce: r x read c
             alg_bytes = 4 * d_pad * (5 * r + (4 if mode == "fused" else 2))
         if args.tau != 1 and not learner:   # mix of sync rounds and local-only iterations
@@ -497,6 +510,10 @@ def main():
                     "rs_bus_gbs": bus(s_rs), "ag_bus_gbs": bus(s_ag),
                     "bus_gbs": s_comb, "frac": (s_comb / NVLINK_PEAK_GBS) if s_comb else None,
                     "note": "separate Mode-A handle, same workload, z-sync not overlapped"}
+        if shared:
+            line["config"]["shared_gpu_test"] = ("all ranks time-share cuda:0 "
+                                                 "(SMA_BENCH_SHARED_GPU): a code-path test, not a "
+                                                 "multi-GPU measurement")
         if e2e:
             line["e2e"] = e2e
         if args.tau != 1:
