@@ -292,7 +292,13 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
     return e;
   const dim3 g1(r, (hidden + kHidUnits - 1) / kHidUnits), gL(r, b), g2(r, kHeadSplit),
       g3(r, (hidden + kUnits - 1) / kUnits, (in_dim + kFeat - 1) / kFeat);
-  mlp_hidden_kernel<<<g1, kMlpThreads, sm1, s>>>(X, perm, pos0, b, in_dim, hidden, W, ld, j0, A1);
+  // layer 1 on the tensor cores (sma_learner_mlp_tc.cu) where the shape allows,
+  // else the SIMT kernel; both write the same A1 contract
+  e = launch_mlp_hidden_tc(X, perm, pos0, b, in_dim, hidden, W, ld, r, j0, A1, s);
+  if (e == cudaErrorNotSupported)
+    mlp_hidden_kernel<<<g1, kMlpThreads, sm1, s>>>(X, perm, pos0, b, in_dim, hidden, W, ld, j0, A1);
+  else if (e != cudaSuccess)
+    return e;
   mlp_logits_kernel<<<gL, kMlpThreads, smL, s>>>(y, perm, pos0, b, in_dim, hidden, classes, W, ld,
                                                  j0, A1, E);
   mlp_head_kernel<<<g2, kMlpThreads, sm2, s>>>(b, in_dim, hidden, classes, W, ld, A1, E, DA, G);

@@ -688,3 +688,35 @@ def test_learner_step_overlapped_zsync(torch_cuda, S, orc, kind, variant):
             assert relerr(hs[0].central(), st.z) <= TOL
     for h in hs:
         h.close()
+
+
+@pytest.mark.parametrize("k,b", [(3, 16), (9, 16), (4, 5)])
+def test_mlp_layer1_tensor_cores_vs_simt_and_oracle(torch_cuda, orc, tmp_path, k, b):
+    """NEXT-2: the MLP's layer-1 GEMM on tcgen05 (3xTF32 + |.|-bound MMAs, K split
+    over a 7-CTA cluster; SMA_MLP_TC=1) and the SIMT kernel (SMA_MLP_TC=0) give
+    the same gradients to ~1e-7 and both match the fp64 oracle < 2e-6 (ragged
+    batch b = 5 pads N = 16 with zero rows); the ReLU mask is decided at
+    fp64-level accuracy on both paths (R18)."""
+    import os
+    import subprocess
+    import sys
+    worker = os.path.join(os.path.dirname(__file__), "mlp_grad_worker.py")
+    X, y = sma_inputs.blobs(2_000, seed=12)
+    rnd, seed = 7, 31
+    got = {}
+    for tc in ("0", "1"):
+        out = str(tmp_path / f"g{tc}.npy")
+        env = dict(os.environ, SMA_MLP_TC=tc)
+        subprocess.check_call([sys.executable, worker, out, str(k), str(b), str(rnd), str(seed)],
+                              env=env, timeout=300)
+        got[tc] = np.load(out)
+    d = MLP_D
+    w0 = np.random.default_rng(seed).normal(0, 0.05, d)
+    w0 = w0.astype(np.float32).astype(np.float64)
+    for j in range(k):
+        rows = orc.batch_indices(X.shape[0], k, b, 21, rnd, j)
+        _, gref, margin = orc.mlp_loss_grad(X, y, rows, w0)
+        assert margin > 1e-9
+        for tc in ("0", "1"):
+            assert np.max(np.abs(got[tc][j] - gref)) < 2e-6, (tc, j)
+    assert np.max(np.abs(got["0"] - got["1"])) < 1e-6
