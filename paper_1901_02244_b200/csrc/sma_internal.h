@@ -100,6 +100,11 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
 cudaError_t launch_mlp_hidden_tc(const float* X, const int32_t* perm, int64_t pos0, int b,
                                  int in_dim, int hidden, const float* W, int64_t ld, int r, int j0,
                                  float2* A1, cudaStream_t s);
+// MLP dW1 = da1^T X / b on tcgen05 (3xTF32, M128 x N112 tiles); same
+// cudaErrorNotSupported contract.
+cudaError_t launch_mlp_w1_tc(const float* X, const int32_t* perm, int64_t pos0, int b, int in_dim,
+                             int hidden, int j0, int64_t ld, int r, const float* DA, float* G,
+                             cudaStream_t s);
 // Broadcast: dst rows [r][ld] := src [ld]   and   y := x   (restart / init).
 cudaError_t launch_broadcast_rows(float* dst, int64_t ld, int r, const float* src, int64_t n4,
                                   int num_sms, cudaStream_t s);

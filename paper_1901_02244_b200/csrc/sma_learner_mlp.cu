@@ -302,7 +302,11 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
   mlp_logits_kernel<<<gL, kMlpThreads, smL, s>>>(y, perm, pos0, b, in_dim, hidden, classes, W, ld,
                                                  j0, A1, E);
   mlp_head_kernel<<<g2, kMlpThreads, sm2, s>>>(b, in_dim, hidden, classes, W, ld, A1, E, DA, G);
-  mlp_w1_kernel<<<g3, kMlpThreads, sm3, s>>>(X, perm, pos0, b, in_dim, hidden, j0, ld, DA, G);
+  e = launch_mlp_w1_tc(X, perm, pos0, b, in_dim, hidden, j0, ld, r, DA, G, s);
+  if (e == cudaErrorNotSupported)
+    mlp_w1_kernel<<<g3, kMlpThreads, sm3, s>>>(X, perm, pos0, b, in_dim, hidden, j0, ld, DA, G);
+  else if (e != cudaSuccess)
+    return e;
   return cudaGetLastError();
 }
 

@@ -358,6 +358,151 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_hidden_tc_kernel(
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
 }
 
+
+// ------------------------------------------------------------------- dW1
+// dW1[u][f] = (1/b) sum_t da1[t][u] x_t[f] (back-propagation into layer 1,
+// PAPER.md:249-256; batch mean, Eq. 2) as D[u][f] = A[u][:] . B[f][:] with
+// M = 128 units, N = 112 features, K = the batch (zero-padded to 32, one
+// 128-byte swizzle atom): A[u][t] = da1[t][u], B[f][t] = x_t[f], both staged
+// K-major by the threads (a transpose of the tiny da1 / X tiles), 3xTF32 split,
+// three tcgen05.mma per K step into 112 TMEM columns; the epilogue reads 16
+// columns per tcgen05.ld and writes rows of dW1 with 128-bit stores.  No cluster:
+// K is the batch, so each CTA owns a whole output tile.  db1 on the f0 = 0 CTAs.
+constexpr int kW1N = 112;                              // UMMA N (features per CTA)
+constexpr int kW1ABytes = kTcM * kBoxK * 4;            // 16 KB
+constexpr int kW1BBytes = kW1N * kBoxK * 4;            // 14 KB
+constexpr int kW1Smem = 2 * kW1ABytes + 2 * kW1BBytes + 1024 + 64;
+constexpr uint32_t kIdescW1 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(kW1N >> 3) << 17) |
+                              ((uint32_t)(kTcM >> 4) << 24);
+
+__global__ void __launch_bounds__(kTcThreads) mlp_w1_tc_kernel(
+    const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
+    int hidden, int j0, int64_t ld, const float* __restrict__ DA, float* __restrict__ Gall) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* Ah = sm;
+  uint8_t* Al = sm + kW1ABytes;
+  uint8_t* Bh = sm + 2 * kW1ABytes;
+  uint8_t* Bl = Bh + kW1BBytes;
+  uint8_t* ctl = Bl + kW1BBytes;
+  uint64_t* bar_mma = reinterpret_cast<uint64_t*>(ctl);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ctl + 8);
+  const int f0 = blockIdx.x * kW1N, mt = blockIdx.y, slot = blockIdx.z;
+  const int u0 = mt * kTcM;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int32_t* prow = perm + pos0 + (int64_t)(j0 + slot) * b;
+  const float* da = DA + (int64_t)slot * b * hidden;
+
+  if (threadIdx.x == 32) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar_mma)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {  // 128 TMEM columns (>= N = 112)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                     smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  // A[u][t] = da1[t][u0 + u] (coalesced along u), B[f][t] = x_t[f0 + f]; every
+  // thread issues all of its loads before the first use (one memory latency)
+  constexpr int kAE = kTcM * kBoxK / kTcThreads, kBE = kW1N * kBoxK / kTcThreads;
+  static_assert(kAE * kTcThreads == kTcM * kBoxK && kBE * kTcThreads == kW1N * kBoxK, "tiling");
+  float av[kAE], bv[kBE];
+#pragma unroll
+  for (int i = 0; i < kAE; ++i) {
+    const int e = threadIdx.x + i * kTcThreads;
+    const int t = e / kTcM, u = e - t * kTcM;
+    av[i] = t < b ? __ldg(da + (int64_t)t * hidden + u0 + u) : 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < kBE; ++i) {
+    const int e = threadIdx.x + i * kTcThreads;
+    const int t = e / kW1N, f = e - t * kW1N;
+    bv[i] = (t < b && f0 + f < in_dim) ? __ldg(X + (int64_t)__ldg(prow + t) * in_dim + f0 + f) : 0.f;
+  }
+#pragma unroll
+  for (int i = 0; i < kAE; ++i) {
+    const int e = threadIdx.x + i * kTcThreads;
+    const int t = e / kTcM, u = e - t * kTcM;
+    const float h = rna_tf32(av[i]);
+    const uint32_t off = sw128_off(u, t);
+    *reinterpret_cast<float*>(Ah + off) = h;
+    *reinterpret_cast<float*>(Al + off) = rna_tf32(__fsub_rn(av[i], h));
+  }
+#pragma unroll
+  for (int i = 0; i < kBE; ++i) {
+    const int e = threadIdx.x + i * kTcThreads;
+    const int t = e / kW1N, f = e - t * kW1N;
+    const float h = rna_tf32(bv[i]);
+    const uint32_t off = sw128_off(f, t);
+    *reinterpret_cast<float*>(Bh + off) = h;
+    *reinterpret_cast<float*>(Bl + off) = rna_tf32(__fsub_rn(bv[i], h));
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) {
+    const uint32_t a0 = smem_u32(Ah), al0 = smem_u32(Al), b0 = smem_u32(Bh), bl0 = smem_u32(Bl);
+    const int nstep = (b + 7) / 8;
+    for (int s = 0; s < nstep; ++s) {
+      const uint32_t o = (uint32_t)s * 32u;
+      const uint32_t acc = s > 0;
+      asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                   "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                   "l"(sw128_desc(a0 + o)), "l"(sw128_desc(b0 + o)), "r"(kIdescW1), "r"(acc));
+      asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem),
+                   "l"(sw128_desc(a0 + o)), "l"(sw128_desc(bl0 + o)), "r"(kIdescW1));
+      asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem),
+                   "l"(sw128_desc(al0 + o)), "l"(sw128_desc(b0 + o)), "r"(kIdescW1));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar_mma))
+                 : "memory");
+  }
+  float* G = Gall + (int64_t)slot * ld;
+  const float fb = (float)b;
+  if (blockIdx.x == 0 && threadIdx.x < kTcM) {  // db1 = (1/b) sum_t da1[t][u]
+    float s = 0.f;
+    for (int t = 0; t < b; ++t) s = __fadd_rn(s, da[(int64_t)t * hidden + u0 + threadIdx.x]);
+    G[(int64_t)hidden * in_dim + u0 + threadIdx.x] = __fdiv_rn(s, fb);
+  }
+  mbar_wait(bar_mma, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // warp w reads TMEM lanes 32 (w % 4) .. +31 (one unit row per lane), column
+  // chunks w / 4, w / 4 + 2, ... of 16
+  const int u = u0 + (warp & 3) * 32 + lane;
+  float* grow = G + (int64_t)u * in_dim;
+  for (int c = warp >> 2; c < kW1N / 16; c += 2) {
+    uint32_t v[16];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+        "%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(c * 16)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int fc = f0 + c * 16;
+    if (fc + 16 <= in_dim) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        reinterpret_cast<float4*>(grow + fc)[i] =
+            make_float4(__fdiv_rn(__uint_as_float(v[4 * i + 0]), fb),
+                        __fdiv_rn(__uint_as_float(v[4 * i + 1]), fb),
+                        __fdiv_rn(__uint_as_float(v[4 * i + 2]), fb),
+                        __fdiv_rn(__uint_as_float(v[4 * i + 3]), fb));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (fc + i < in_dim) grow[fc + i] = __fdiv_rn(__uint_as_float(v[i]), fb);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
 // ---------------------------------------------------------------- host side
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                    const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -366,9 +511,11 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 EncodeTiledFn g_encode = nullptr;
 std::once_flag g_encode_once;
 
-// SMA_MLP_TC: 0 = SIMT kernel, 1 = tensor cores, unset = by learners per GPU:
-// measured (profiles/r01_mlp_tc_sweep.txt, MLP rounds/s, b = 16) the tensor-core
-// layer is 1.5-5 % slower at r <= 4 and 2-4.5 % faster at r >= 8.
+// SMA_MLP_TC: 0 = SIMT kernels, 1 = tensor cores, unset = by learners per GPU:
+// measured (profiles/r01_mlp_tc_sweep.txt, MLP rounds/s, b = 16) the two
+// tensor-core GEMMs (layer 1 + dW1) are 12-19 % slower at r <= 4 (56 CTAs of
+// short latency phases vs the SIMT kernels' 256-832) and 3 / 19 / 23 % faster at
+// r = 8 / 16 / 32.
 int tc_policy() {
   static const int p = [] {
     const char* e = getenv("SMA_MLP_TC");
@@ -426,4 +573,23 @@ cudaError_t launch_mlp_hidden_tc(const float* X, const int32_t* perm, int64_t po
                             j0, A1);
 }
 
+}  // namespace sma
+
+namespace sma {
+// dW1 on tcgen05; cudaErrorNotSupported (nothing launched) when the policy or
+// the shape keeps it on the SIMT kernel (b > 32, hidden % 128, in_dim % 4).
+cudaError_t launch_mlp_w1_tc(const float* X, const int32_t* perm, int64_t pos0, int b, int in_dim,
+                             int hidden, int j0, int64_t ld, int r, const float* DA, float* G,
+                             cudaStream_t s) {
+  const int pol = tc_policy();
+  if (pol == 0 || (pol < 0 && r < 8) || b < 1 || b > kBoxK || hidden % kTcM != 0 ||
+      (in_dim & 3) != 0 || r < 1)
+    return cudaErrorNotSupported;
+  cudaError_t e = cudaFuncSetAttribute(mlp_w1_tc_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kW1Smem);
+  if (e != cudaSuccess) return e;
+  const dim3 grid((in_dim + kW1N - 1) / kW1N, hidden / kTcM, r);
+  mlp_w1_tc_kernel<<<grid, kTcThreads, kW1Smem, s>>>(X, perm, pos0, b, in_dim, hidden, j0, ld, DA, G);
+  return cudaGetLastError();
+}
 }  // namespace sma
