@@ -34,6 +34,7 @@ def sources() -> list[str]:
 
 def deps() -> list[str]:
     return sources() + sorted(glob.glob(os.path.join(CSRC, "*.h"))) + \
+        sorted(glob.glob(os.path.join(CSRC, "*.cuh"))) + \
         [os.path.join(ROOT, "include", "sma.h")]
 
 

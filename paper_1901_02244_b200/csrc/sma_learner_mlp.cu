@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include "sma_bulk.cuh"
+#include "sma_dot2.cuh"
 #include "sma_internal.h"
 
 namespace sma {
@@ -31,31 +32,9 @@ __device__ __forceinline__ int batch_row(const int32_t* perm, int64_t pos0, int 
   return perm[pos0 + (int64_t)j * b + t];
 }
 
-// Error-free transformations (Knuth TwoSum, FMA TwoProd): the Ogita-Rump-Oishi
-// "Dot2" accumulation gives a dot product as accurate as one computed in twice
-// the working precision (~2^-48), with fp32 instructions only (the F2F
-// conversions of a plain fp64 accumulation were the bottleneck: profiles/).
-struct f2 { float hi, lo; };
-__device__ __forceinline__ void two_sum(float a, float b, float& s, float& e) {
-  s = __fadd_rn(a, b);
-  const float bb = __fsub_rn(s, a);
-  e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
-}
-__device__ __forceinline__ void dot2_step(f2& acc, float w, float x) {
-  const float p = __fmul_rn(w, x);
-  const float pe = __fmaf_rn(w, x, -p);        // exact: w*x = p + pe
-  float s, e;
-  two_sum(acc.hi, p, s, e);
-  acc.hi = s;
-  acc.lo = __fadd_rn(acc.lo, __fadd_rn(e, pe));
-}
-__device__ __forceinline__ f2 f2_add(f2 a, f2 b) {
-  f2 r;
-  float e;
-  two_sum(a.hi, b.hi, r.hi, e);
-  r.lo = __fadd_rn(__fadd_rn(a.lo, b.lo), e);
-  return r;
-}
+using dot2::f2;
+using dot2::dot2_step;
+using dot2::f2_add;
 
 __global__ void __launch_bounds__(kMlpThreads) mlp_hidden_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
@@ -129,14 +108,7 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_hidden_kernel(
       } else {
         for (int f = lane; f < in_dim; f += 32) dot2_step(acc, w[f], x[f]);
       }
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) {
-        f2 o;
-        o.hi = __shfl_xor_sync(0xffffffffu, acc.hi, off);
-        o.lo = __shfl_xor_sync(0xffffffffu, acc.lo, off);
-        acc = f2_add(acc, o);
-      }
-      acc = f2_add(acc, f2{bias, 0.f});
+      acc = f2_add(dot2::warp_sum(acc), f2{bias, 0.f});
     }
     if (lane == 0) A1[((int64_t)slot * b + t) * hidden + k0 + u] = make_float2(acc.hi, acc.lo);
   }

@@ -40,6 +40,7 @@
 
 #include <mutex>
 
+#include "sma_dot2.cuh"
 #include "sma_internal.h"
 
 namespace sma {
@@ -107,27 +108,9 @@ __device__ __forceinline__ uint32_t sw128_off(int row, int k) {
   return (uint32_t)row * 128u + ((uint32_t)(((k >> 2) ^ (row & 7))) << 4) + (uint32_t)(k & 3) * 4u;
 }
 
-struct f2 { float hi, lo; };
-__device__ __forceinline__ void two_sum(float a, float b, float& s, float& e) {
-  s = __fadd_rn(a, b);
-  const float bb = __fsub_rn(s, a);
-  e = __fadd_rn(__fsub_rn(a, __fsub_rn(s, bb)), __fsub_rn(b, bb));
-}
-__device__ __forceinline__ void dot2_step(f2& acc, float w, float x) {
-  const float p = __fmul_rn(w, x);
-  const float pe = __fmaf_rn(w, x, -p);
-  float s, e;
-  two_sum(acc.hi, p, s, e);
-  acc.hi = s;
-  acc.lo = __fadd_rn(acc.lo, __fadd_rn(e, pe));
-}
-__device__ __forceinline__ f2 f2_add(f2 a, f2 b) {
-  f2 r;
-  float e;
-  two_sum(a.hi, b.hi, r.hi, e);
-  r.lo = __fadd_rn(__fadd_rn(a.lo, b.lo), e);
-  return r;
-}
+using dot2::f2;
+using dot2::dot2_step;
+using dot2::f2_add;
 
 __global__ void __launch_bounds__(kTcThreads, 1) mlp_hidden_tc_kernel(
     const __grid_constant__ CUtensorMap tmW1, const float* __restrict__ X,
@@ -343,14 +326,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_hidden_tc_kernel(
       const float* x = X + (int64_t)rows[t] * in_dim;
       f2 acc = {0.f, 0.f};
       for (int f = lane; f < in_dim; f += 32) dot2_step(acc, __ldg(w + f), __ldg(x + f));
-#pragma unroll
-      for (int off = 16; off >= 1; off >>= 1) {
-        f2 o;
-        o.hi = __shfl_xor_sync(0xffffffffu, acc.hi, off);
-        o.lo = __shfl_xor_sync(0xffffffffu, acc.lo, off);
-        acc = f2_add(acc, o);
-      }
-      acc = f2_add(acc, f2{b1[u], 0.f});
+      acc = f2_add(dot2::warp_sum(acc), f2{b1[u], 0.f});
       if (lane == 0) A1[((int64_t)slot * b + t) * hidden + u] = make_float2(acc.hi, acc.lo);
     }
   }
