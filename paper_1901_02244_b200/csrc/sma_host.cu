@@ -9,9 +9,11 @@
 
 #include <mutex>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "sma_host.h"
+#include "sma_internal.h"
 
 using namespace sma;
 
@@ -173,3 +175,25 @@ extern "C" sma_status sma_autotune_step(int32_t m, double tau, const double* t, 
   return SMA_OK;
 }
 
+
+// ------------------------------------------------ dynamic shared memory cache
+namespace sma {
+cudaError_t ensure_dyn_smem(const void* func, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<const void*, int>, int>> done;  // (func, dev) -> bytes
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& kv : done)
+    if (kv.first.first == func && kv.first.second == dev) {
+      if (kv.second >= bytes) return cudaSuccess;
+      e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+      if (e == cudaSuccess) kv.second = bytes;
+      return e;
+    }
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.push_back({{func, dev}, bytes});
+  return e;
+}
+}  // namespace sma

@@ -52,6 +52,11 @@ struct ReplicaArgs {
   float alpha_g;       // kHierA/B: inter-GPU correction weight
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) only when the size
+// grows for this (kernel, device): the call costs microseconds of host time and
+// the learner launchers would otherwise issue it on every round.  Thread-safe.
+cudaError_t ensure_dyn_smem(const void* func, int bytes);
+
 // Launchers (return the launch error, never synchronise).
 cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a, int num_sms,
                                 cudaStream_t s);

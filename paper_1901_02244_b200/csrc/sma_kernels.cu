@@ -864,8 +864,7 @@ cudaError_t launch_softmax_grad(const float* X, const int32_t* y, const int32_t*
   if (classes > kMaxClasses || b > 64) return cudaErrorInvalidValue;
   const size_t sm1 = sizeof(float) * (size_t)in_dim;
   const size_t sm2 = sizeof(float) * ((size_t)b * kFeat + (size_t)b * classes);
-  cudaError_t e = cudaFuncSetAttribute(softmax_logits_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(softmax_logits_kernel), (int)sm1);
   if (e != cudaSuccess) return e;
   softmax_logits_kernel<<<dim3(r, b), classes * 32, sm1, s>>>(X, y, perm, pos0, b, in_dim, classes, W,
                                                               ld, j0, E);
@@ -883,11 +882,9 @@ cudaError_t launch_softmax_round(const float* X, const int32_t* y, const int32_t
   const size_t sm2 = sizeof(float) * ((size_t)a.r * b * kFeatF + (size_t)a.r * b * classes) +
                      sizeof(int) * (size_t)a.r * b;
   if (sm2 > 200 * 1024) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(softmax_logits_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm1);
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(softmax_logits_kernel), (int)sm1);
   if (e != cudaSuccess) return e;
-  if ((e = cudaFuncSetAttribute(softmax_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sm2)) != cudaSuccess)
+  if ((e = ensure_dyn_smem(reinterpret_cast<const void*>(softmax_round_kernel), (int)sm2)) != cudaSuccess)
     return e;
   softmax_logits_kernel<<<dim3(a.r, b), classes * 32, sm1, s>>>(X, y, perm, pos0, b, in_dim, classes,
                                                                 a.W, a.ld, j0, E);

@@ -219,7 +219,7 @@ template <int MODE, int TILE, int STAGES>
 cudaError_t launch_mode(const ReplicaArgs& a, int64_t ntiles, int num_sms, cudaStream_t s) {
   auto k = replica_step_tma<MODE, TILE, STAGES>;
   const int smem = (int)sizeof(TmaSmem<TILE, STAGES>);
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(k), smem);
   if (e != cudaSuccess) return e;
   int occ = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k, kThreadsTma, smem) != cudaSuccess ||

@@ -256,11 +256,9 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
                      16 + sizeof(float2) * (size_t)b * hidden;
   const size_t sm3 = sizeof(float) * ((size_t)b * kFeat + (size_t)b * kUnits);
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(mlp_hidden_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sm1)) != cudaSuccess)
+  if ((e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_hidden_kernel), (int)sm1)) != cudaSuccess)
     return e;
-  if ((e = cudaFuncSetAttribute(mlp_head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sm2)) != cudaSuccess)
+  if ((e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_head_kernel), (int)sm2)) != cudaSuccess)
     return e;
   const dim3 g1(r, (hidden + kHidUnits - 1) / kHidUnits), gL(r, b), g2(r, kHeadSplit),
       g3(r, (hidden + kUnits - 1) / kUnits, (in_dim + kFeat - 1) / kFeat);

@@ -519,18 +519,33 @@ cudaError_t launch_mlp_hidden_tc(const float* X, const int32_t* perm, int64_t po
       g_encode = reinterpret_cast<EncodeTiledFn>(p);
   });
   if (!g_encode) return cudaErrorNotSupported;
-  // W [r][ld] with W1 = [hidden][in_dim] at the start of each replica
-  CUtensorMap tm;
-  const cuuint64_t dims[3] = {(cuuint64_t)in_dim, (cuuint64_t)hidden, (cuuint64_t)r};
-  const cuuint64_t strides[2] = {(cuuint64_t)in_dim * 4, (cuuint64_t)ld * 4};
-  const cuuint32_t box[3] = {kBoxK, kTcM, 1};
-  const cuuint32_t estr[3] = {1, 1, 1};
-  if (g_encode(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(W), dims, strides, box,
-               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(mlp_hidden_tc_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+  // W [r][ld] with W1 = [hidden][in_dim] at the start of each replica; the
+  // encoded map is cached per issuing thread (re-encoded when W or a shape changes)
+  struct MapCache {
+    const float* W = nullptr;
+    int64_t ld = 0;
+    int r = 0, in_dim = 0, hidden = 0;
+    CUtensorMap tm;
+  };
+  thread_local MapCache mc;
+  if (mc.W != W || mc.ld != ld || mc.r != r || mc.in_dim != in_dim || mc.hidden != hidden) {
+    const cuuint64_t dims[3] = {(cuuint64_t)in_dim, (cuuint64_t)hidden, (cuuint64_t)r};
+    const cuuint64_t strides[2] = {(cuuint64_t)in_dim * 4, (cuuint64_t)ld * 4};
+    const cuuint32_t box[3] = {kBoxK, kTcM, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    mc.W = nullptr;
+    if (g_encode(&mc.tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(W), dims, strides,
+                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorNotSupported;
+    mc.W = W;
+    mc.ld = ld;
+    mc.r = r;
+    mc.in_dim = in_dim;
+    mc.hidden = hidden;
+  }
+  const CUtensorMap& tm = mc.tm;
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_hidden_tc_kernel), kSmemBytes);
   if (e != cudaSuccess) return e;
   const int nks = (in_dim + kTcKC - 1) / kTcKC;
   cudaLaunchConfig_t cfg = {};
@@ -561,8 +576,7 @@ cudaError_t launch_mlp_w1_tc(const float* X, const int32_t* perm, int64_t pos0, 
   if (pol == 0 || (pol < 0 && r < 8) || b < 1 || b > kBoxK || hidden % kTcM != 0 ||
       (in_dim & 3) != 0 || r < 1)
     return cudaErrorNotSupported;
-  cudaError_t e = cudaFuncSetAttribute(mlp_w1_tc_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kW1Smem);
+  cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_w1_tc_kernel), kW1Smem);
   if (e != cudaSuccess) return e;
   const dim3 grid((in_dim + kW1N - 1) / kW1N, hidden / kTcM, r);
   mlp_w1_tc_kernel<<<grid, kTcThreads, kW1Smem, s>>>(X, perm, pos0, b, in_dim, hidden, j0, ld, DA, G);
