@@ -183,3 +183,96 @@ def test_p2p_hierarchical_dyadic_bitwise(tmp_path, world, k, mode):
         assert np.load(tmp_path / f"u{g}.npy").tolist() == [float(v) for v in U[g]], g
     for j in range(k):
         assert np.load(tmp_path / f"w{j}.npy").tolist() == [float(v) for v in W[j]], j
+
+
+def _hier_ckpt_worker(rank, world, port, flags, d, k, out):
+    """Two-level rule over 3 phases: 5 rounds; checkpoint every vector
+    (replicas, u_g, z, z_prev), 2 more rounds, restore the checkpoint (so those
+    2 rounds are undone) and change alpha_g; 2 local-only iterations (tau);
+    restart (replicas, u_g, z_prev := z); 3 more rounds."""
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+
+    import sma_inputs
+    from paper_1901_02244_b200 import sma
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    al, g, m = (float(np.float32(x)) for x in (0.25, 0.1, 0.9))
+    h = sma.Sma(d, k, al, g, m, sma_inputs.w0(d), rank=rank, world=world, device=0,
+                flags=flags | sma.FLAG_P2P_ZSYNC | sma.FLAG_HIERARCHICAL)
+    handles = [None] * world
+    dist.all_gather_object(handles, sma.sma_p2p_handle(h.h))
+    sma.sma_p2p_connect(h.h, handles)
+    dist.barrier()
+    s = torch.cuda.Stream()
+
+    def rnd(i, local=False):
+        h.synth_grads(i, sma_inputs.SEED_G, s)
+        (h.step_local if local else h.step)(s)
+
+    for i in range(5):
+        rnd(i)
+    s.synchronize()
+    ck = (h.central(), h.central_prev(), [h.replica(j) for j in h.local_replicas()],
+          h.reference() if rank else None)
+    for i in range(5, 7):
+        rnd(i)
+    s.synchronize()
+    dist.barrier()
+    h.set_central(ck[0], ck[1])
+    for j, w in zip(h.local_replicas(), ck[2]):
+        h.set_replica(j, w)
+    if rank:
+        h.set_reference(ck[3])
+    h.set_alpha_global(float(np.float32(0.125)))
+    dist.barrier()
+    for i in range(7, 9):
+        rnd(i, local=True)
+    h.restart(s)
+    for i in range(9, 12):
+        rnd(i)
+    s.synchronize()
+    np.save(os.path.join(out, f"z{rank}.npy"), h.central())
+    np.save(os.path.join(out, f"u{rank}.npy"), h.reference())
+    for j in h.local_replicas():
+        np.save(os.path.join(out, f"w{j}.npy"), h.replica(j))
+    dist.barrier()
+    h.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["A", "B"])
+def test_p2p_hierarchical_checkpoint_tau_restart(orc, tmp_path, mode):
+    """Checkpoint / restore of the complete two-level state (sma_get/set_reference
+    with the central model and the replicas), alpha_g changed between rounds,
+    tau-periodic local iterations (R17) and restart, 3 ranks / 7 learners, vs the
+    two-level oracle driven through the same sequence."""
+    import torch.multiprocessing as mp
+
+    import sma_inputs
+    world, k, d = 3, 7, 20_011
+    mp.spawn(_hier_ckpt_worker, args=(world, _port(), {"A": 0, "B": 1}[mode], d, k,
+                                      str(tmp_path)), nprocs=world)
+    f = lambda x: float(np.float32(x))  # noqa: E731
+    al, g, m = f(0.25), f(0.1), f(0.9)
+    G = lambda i: np.stack([sma_inputs.grad(i, j, k, d) for j in range(k)])  # noqa: E731
+    st = orc.HierState.init(sma_inputs.w0(d), k, world)
+    for i in range(5):
+        st.round(G(i), al, f(1 / (2 * (world - 1))), g, m)
+    ag = f(0.125)
+    for i in range(7, 9):  # local-only iterations: w_j -= gamma g_j
+        st.W = st.W - g * G(i)
+    st.W[:] = st.z                         # restart: replicas, u_g, z_prev := z
+    st.U[:] = st.z
+    st.z_prev = st.z.copy()
+    for i in range(9, 12):
+        st.round(G(i), al, ag, g, m)
+    rel = lambda x, y: np.max(np.abs(x - y) / (1 + np.abs(y)))  # noqa: E731
+    assert rel(np.load(tmp_path / "z0.npy"), st.z) <= 1e-5
+    for r in range(world):
+        assert rel(np.load(tmp_path / f"u{r}.npy"), st.U[r]) <= 1e-5
+    for j in range(k):
+        assert rel(np.load(tmp_path / f"w{j}.npy"), st.W[j]) <= 1e-5
