@@ -452,8 +452,10 @@ def main():
             kname += " / replica_step_ldg<kLocal>"
         achieved = alg_bytes / (kern_avg * 1e-3) / 1e9
         traffic = None
-        tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_n{world}_{mode}_{kvar}.json")
-        if os.path.exists(tpath):
+        # the per-GPU replica kernel depends on (config, r, mode, kernel) only, so the
+        # capture of r replicas on one GPU also serves N = k/r GPUs
+        tpath = os.path.join(ROOT, "profiles", f"traffic_{args.config}_r{r}_{mode}_{kvar}.json")
+        if os.path.exists(tpath) and not (args.matc or args.hier or args.tau != 1):
             try:
                 traffic = json.load(open(tpath)).get("dram_bytes_per_launch")
             except Exception:
