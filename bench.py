@@ -131,6 +131,19 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
+def host_info():
+    """The host the oracle ran on: online cores and the CPU model (/proc/cpuinfo)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
 def cpu_baseline(d, k, alpha, gamma, mu, n_idx=1 << 23, rounds=10):
     """The oracle as it stands (single thread, fp64), on a bounded sample of
     the same workload: all k replicas, `rounds` rounds, n_idx seeded parameter
@@ -147,6 +160,7 @@ def cpu_baseline(d, k, alpha, gamma, mu, n_idx=1 << 23, rounds=10):
                      want_W=False)
     dt = time.perf_counter() - t
     return {"value": rounds * (n_idx / d) / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "host": host_info(),
             "sample": f"{rounds} full SMA rounds (k={k}) over {n_idx} of d={d} parameter "
                       f"indices, fp64 single-thread C oracle, {dt:.1f} s"}
 
@@ -187,6 +201,7 @@ def run_reference(args):
             "config": {"workload": workload_name(args.config, d, k).replace(
                            "fp32", "the fp64 CPU oracle on a bounded sample"), "d": d, "k": k},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "host": host_info(),
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
