@@ -371,6 +371,14 @@ enum { SMA_PHASE_REPLICA = 0, SMA_PHASE_REDUCE_SCATTER = 1, SMA_PHASE_SHARD_UPDA
 sma_status sma_kernel_time(sma_handle* h, int32_t phase, double* total_ms, int64_t* launches,
                            int reset);
 
+/* Turn the per-phase CUDA events of SMA_FLAG_TIMING on or off between calls
+ * (the flag sets the initial state).  The events cost GPU time between the
+ * kernels of a round (~2.5 us each on B200, a third of a small round), so a
+ * benchmark times its rounds with them off and measures the per-phase
+ * durations in a separate pass with them on.  While timing is on, rounds are
+ * not run as CUDA graphs.  Errors: INVALID_ARG. */
+sma_status sma_set_timing(sma_handle* h, int on);
+
 /* Number of libsma CUDA kernels this handle has launched (NCCL collectives not counted). */
 int64_t sma_launch_count(const sma_handle* h);
 

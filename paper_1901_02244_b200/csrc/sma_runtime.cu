@@ -471,7 +471,7 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
   if ((f & SMA_FLAG_KERNEL_TMA) && (f & SMA_FLAG_KERNEL_LDG))
     return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_KERNEL_TMA and SMA_FLAG_KERNEL_LDG are exclusive");
   h->timing = (f & SMA_FLAG_TIMING) != 0;
-  h->graphs = (f & SMA_FLAG_CUDA_GRAPH) != 0 && !h->timing;
+  h->graphs = (f & SMA_FLAG_CUDA_GRAPH) != 0;  // used only while timing is off
   h->check = (f & SMA_FLAG_CHECK_FINITE) != 0;
   h->nvls = (f & SMA_FLAG_NVLS_ZSYNC) != 0;
   h->p2p = (f & SMA_FLAG_P2P_ZSYNC) != 0;
@@ -723,7 +723,7 @@ sma_status sma_step(sma_handle* h, void* stream) {
     ++h->launches;
     h->q_dirty = false;
   }
-  if (h->graphs && s != nullptr) {
+  if (h->graphs && !h->timing && s != nullptr) {
     const int key = h->cur;
     if (!h->gexec[key] || h->gver[key] != h->ver) {
       const int64_t launches0 = h->launches;
@@ -1093,8 +1093,8 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
   const size_t fused_smem =
       (sizeof(float) * (32 + (size_t)h->classes) + sizeof(int)) * (size_t)h->r * h->batch;
   const bool fusable = h->kind == 0 && !h->collective && !h->matc && h->r > 0 &&
-                       h->classes <= 16 && fused_smem <= 200 * 1024 && !h->graphs;
-  if (!fusable && h->collective && h->overlap && !h->graphs) {
+                       h->classes <= 16 && fused_smem <= 200 * 1024 && !(h->graphs && !h->timing);
+  if (!fusable && h->collective && h->overlap && !(h->graphs && !h->timing)) {
     // Mode B: the z-sync of this round is forked first and overlaps the
     // learner kernels and the replica kernel
     NvtxRange nvtx2("sma_learner_step.overlap");
@@ -1182,6 +1182,12 @@ sma_status sma_p2p_connect(sma_handle* h, const void* handles) {
     h->p2p_base[g] = static_cast<char*>(p);
   }
   h->p2p_connected = true;
+  return SMA_OK;
+}
+
+sma_status sma_set_timing(sma_handle* h, int on) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  h->timing = on != 0;
   return SMA_OK;
 }
 

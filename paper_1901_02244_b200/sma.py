@@ -46,7 +46,7 @@ EXPORTS = ["sma_create", "sma_destroy", "sma_set_learner_grads", "sma_set_learne
            "sma_launch_count", "sma_info", "sma_last_error", "sma_abi_version",
            "sma_step_local", "sma_autotune_step", "sma_set_local_replicas", "sma_learner_step",
            "sma_p2p_handle", "sma_p2p_connect", "sma_set_alpha_global", "sma_get_reference",
-           "sma_set_reference"]
+           "sma_set_reference", "sma_set_timing"]
 
 
 class SmaError(RuntimeError):
@@ -114,6 +114,7 @@ def load():
         "sma_set_alpha_global": ([P, C.c_float], st),
         "sma_get_reference": ([P, P, C.c_int], st),
         "sma_set_reference": ([P, P, C.c_int], st),
+        "sma_set_timing": ([P, C.c_int], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -327,6 +328,10 @@ def sma_kernel_time(h: int, phase: int = PHASE_REPLICA, reset: bool = False) -> 
     return ms.value, n.value
 
 
+def sma_set_timing(h: int, on: bool) -> None:
+    _check(load().sma_set_timing(h, int(on)), "sma_set_timing")
+
+
 def sma_launch_count(h: int) -> int:
     return int(load().sma_launch_count(h))
 
@@ -450,6 +455,9 @@ class Sma:
 
     def kernel_time(self, reset=False, phase=PHASE_REPLICA):
         return sma_kernel_time(self.h, phase, reset)
+
+    def set_timing(self, on):
+        sma_set_timing(self.h, on)
 
     def launch_count(self):
         return sma_launch_count(self.h)
