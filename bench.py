@@ -260,7 +260,7 @@ def main():
     # A round that is one kernel (the fused n = 1 path) gets its kernel's average
     # launch duration from the timed window itself; otherwise a separate pass
     # with the events on (sma_set_timing) measures the phases.
-    flags = 0
+    flags = sma.FLAG_CUDA_GRAPH if os.environ.get("SMA_BENCH_GRAPH") == "1" else 0
     if collective:
         flags |= sma.FLAG_FORCE_COLLECTIVE
         if mode == "B":

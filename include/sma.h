@@ -309,11 +309,13 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
 sma_status sma_learner_grads(sma_handle* h, int64_t round, void* cuda_stream);
 
 /* One full round with the learner in the loop: exactly sma_learner_grads then
- * sma_step (same results), but for the softmax learner on a single-GPU handle
- * (no MATERIALIZE_C, no CUDA graph) the gradient slice, the replica update and
- * the central update run fused in one kernel after the logits kernel, so the
- * gradient never makes an HBM round trip (the gradient buffers are still
- * written and registered).  Errors: as sma_learner_grads and sma_step. */
+ * sma_step (same results).  Under Mode B the z-sync of the round is forked
+ * before the learner kernels, so it overlaps them.  With the
+ * environment variable SMA_LEARNER_FUSE=1, the softmax learner on a single-GPU
+ * handle (no MATERIALIZE_C, no CUDA graph) runs the gradient slice, the replica
+ * update and the central update fused in one kernel after the logits kernel
+ * (the gradient never makes an HBM round trip; measured slower on B200, so
+ * opt-in).  Errors: as sma_learner_grads and sma_step. */
 sma_status sma_learner_step(sma_handle* h, int64_t round, void* cuda_stream);
 
 /* ------------------------------------------------ bookkeeping (host only) */

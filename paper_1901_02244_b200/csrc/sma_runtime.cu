@@ -1092,7 +1092,13 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
   if (round < 0) return fail(SMA_ERR_INVALID_ARG, "round < 0");
   const size_t fused_smem =
       (sizeof(float) * (32 + (size_t)h->classes) + sizeof(int)) * (size_t)h->r * h->batch;
-  const bool fusable = h->kind == 0 && !h->collective && !h->matc && h->r > 0 &&
+  // The learner-fused softmax round (one kernel after the logits) is opt-in,
+  // SMA_LEARNER_FUSE=1 (read per call): on B200 the unfused sequence (logits,
+  // feature-sliced dW, the small-round replica kernel) measured faster, 58.8k vs
+  // 54.1k C1 rounds/s -- the fused kernel's 26 CTAs serialise its update work.
+  const char* fe = getenv("SMA_LEARNER_FUSE");
+  const bool fuse_knob = fe && fe[0] == '1';
+  const bool fusable = fuse_knob && h->kind == 0 && !h->collective && !h->matc && h->r > 0 &&
                        h->classes <= 16 && fused_smem <= 200 * 1024 && !(h->graphs && !h->timing);
   if (!fusable && h->collective && h->overlap && !(h->graphs && !h->timing)) {
     // Mode B: the z-sync of this round is forked first and overlaps the

@@ -531,6 +531,8 @@ def test_learner_step_fused_is_bitwise_unfused(torch_cuda, S, orc):
     k, b, R = 4, 16, 60
     a, g, m = F32(1 / k), F32(0.1), F32(0.9)
     Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    import os
+    os.environ["SMA_LEARNER_FUSE"] = "1"   # the fused round is opt-in (read per call)
     hs = []
     for fused in (True, False):
         h = S.Sma(7850, k, a, g, m, np.zeros(7850, np.float32))
@@ -543,6 +545,7 @@ def test_learner_step_fused_is_bitwise_unfused(torch_cuda, S, orc):
                 S.sma_learner_grads(h.h, i, s)
                 h.step(s)
         hs.append(h)
+    os.environ.pop("SMA_LEARNER_FUSE")
     assert relerr(hs[0].central(), hs[1].central()) <= 1e-6
     assert relerr(hs[0].central_prev(), hs[1].central_prev()) <= 1e-6
     for j in range(k):
