@@ -12,6 +12,7 @@
 #include <stdlib.h>
 
 #include "sma_bulk.cuh"
+#include "sma_softmax.cuh"
 #include "sma_internal.h"
 
 namespace sma {
@@ -497,6 +498,8 @@ __global__ void __launch_bounds__(kThreads) synth_grads_kernel(float* __restrict
 constexpr int kFeat = 64;
 constexpr int kMaxClasses = 32;
 
+
+
 __global__ void __launch_bounds__(kMaxClasses * 32) softmax_logits_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ y, const int32_t* __restrict__ perm,
     int64_t pos0, int b, int in_dim, int classes, const float* __restrict__ Wall, int64_t ld,
@@ -509,6 +512,8 @@ __global__ void __launch_bounds__(kMaxClasses * 32) softmax_logits_kernel(
   if (threadIdx.x == 0) row_sm = perm[pos0 + (int64_t)(j0 + slot) * b + t];
   __syncthreads();
   const int row = row_sm;
+  // the label, in flight while the row is staged (off the softmax's tail)
+  const int yt0 = threadIdx.x == 0 ? __ldg(y + row) : 0;
   const float* W = Wall + (int64_t)slot * ld;
   const bool vec = (in_dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
   bulk::stage_rows_span(xs, X, &row_sm, 1, in_dim, in_dim, 0, nullptr, nullptr, 0, &bar, 0, true);
@@ -535,16 +540,9 @@ __global__ void __launch_bounds__(kMaxClasses * 32) softmax_logits_kernel(
     if (lane == 0) lg[c] = __fadd_rn(s, W[(int64_t)classes * in_dim + c]);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // max-subtracted softmax of this row, e = p - onehot(y_t)
-    float mx = lg[0];
-    for (int k = 1; k < classes; ++k) mx = fmaxf(mx, lg[k]);
-    float den = 0.f;
-    for (int k = 0; k < classes; ++k) den = __fadd_rn(den, expf(__fsub_rn(lg[k], mx)));
-    const int yt = y[row];
-    float* e = E + ((int64_t)slot * b + t) * classes;
-    for (int k = 0; k < classes; ++k)
-      e[k] = __fsub_rn(__fdiv_rn(expf(__fsub_rn(lg[k], mx)), den), k == yt ? 1.f : 0.f);
-  }
+  if (threadIdx.x < 32)  // max-subtracted softmax of this row, e = p - onehot(y_t)
+    warp_softmax_grad(lg, classes, __shfl_sync(0xffffffffu, yt0, 0),
+                      E + ((int64_t)slot * b + t) * classes);
 }
 
 __global__ void __launch_bounds__(256) softmax_wgrad_kernel(

@@ -19,6 +19,7 @@
 
 #include "sma_bulk.cuh"
 #include "sma_dot2.cuh"
+#include "sma_softmax.cuh"
 #include "sma_internal.h"
 
 namespace sma {
@@ -128,6 +129,8 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_logits_kernel(
   const float* W2 = Wall + (int64_t)slot * ld + (int64_t)hidden * in_dim + hidden;
   const float* b2 = W2 + (int64_t)classes * hidden;
   const float2* a1 = A1 + ((int64_t)slot * b + t) * hidden;
+  __shared__ int yt_sm;
+  if (threadIdx.x == 0) yt_sm = y[batch_row(perm, pos0, j0 + slot, b, t)];  // early: off the tail
   for (int k = threadIdx.x; k < hidden; k += blockDim.x) {  // relu of the double-float a1
     const float2 v = a1[k];
     hrow[k] = (v.x > 0.f || (v.x == 0.f && v.y > 0.f)) ? __fadd_rn(v.x, v.y) : 0.f;
@@ -142,16 +145,8 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_logits_kernel(
     if (lane == 0) lg[c] = __fadd_rn(s, b2[c]);
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    float mx = lg[0];
-    for (int c = 1; c < classes; ++c) mx = fmaxf(mx, lg[c]);
-    float den = 0.f;
-    for (int c = 0; c < classes; ++c) den = __fadd_rn(den, expf(__fsub_rn(lg[c], mx)));
-    const int yt = y[batch_row(perm, pos0, j0 + slot, b, t)];
-    float* e = E + ((int64_t)slot * b + t) * classes;
-    for (int c = 0; c < classes; ++c)
-      e[c] = __fsub_rn(__fdiv_rn(expf(__fsub_rn(lg[c], mx)), den), c == yt ? 1.f : 0.f);
-  }
+  if (threadIdx.x < 32)  // max-subtracted softmax, e = p - onehot(y_t)
+    warp_softmax_grad(lg, classes, yt_sm, E + ((int64_t)slot * b + t) * classes);
 }
 
 // grid (r, kHeadSplit): slices of dW2 = e^T h / b, db2, and
