@@ -489,9 +489,9 @@ std::once_flag g_encode_once;
 
 // SMA_MLP_TC: 0 = SIMT kernels, 1 = tensor cores, unset = by learners per GPU:
 // measured (profiles/r01_mlp_tc_sweep.txt, MLP rounds/s, b = 16) the two
-// tensor-core GEMMs (layer 1 + dW1) are 12-19 % slower at r <= 4 (56 CTAs of
-// short latency phases vs the SIMT kernels' 256-832) and 3 / 19 / 23 % faster at
-// r = 8 / 16 / 32.
+// tensor-core GEMMs (layer 1 + dW1) are 14-22 % slower at r <= 4 (56 CTAs of
+// short latency phases vs the SIMT kernels' 256-832), even at r = 6, and
+// 4 / 10 / 22 / 26 % faster at r = 8 / 12 / 16 / 32.
 int tc_policy() {
   static const int p = [] {
     const char* e = getenv("SMA_MLP_TC");
