@@ -12,6 +12,7 @@
 #include <stdlib.h>
 
 #include "sma_bulk.cuh"
+#include "sma_pdl.cuh"
 #include "sma_softmax.cuh"
 #include "sma_internal.h"
 
@@ -204,6 +205,7 @@ __device__ __forceinline__ void replica_finish(const ReplicaArgs& a, int64_t p0,
 
 template <int MODE, int kUJ, int kMinBlocks = (kUJ >= 8 ? 2 : 4), int POL = 0>
 __global__ void __launch_bounds__(kThreads, kMinBlocks) replica_step_ldg(const ReplicaArgs a) {
+  pdl::wait_and_release();
   const int64_t stride = (int64_t)gridDim.x * kThreads;
   const int64_t dfull4 = a.d >> 2;  // chunks entirely below d: vector path
   const bool matc = a.C != nullptr;
@@ -269,6 +271,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) replica_step_ldg(const R
 // commutative); group 0 finishes the column.  4x the threads for the same d.
 template <int MODE, int G>
 __global__ void __launch_bounds__(kThreads) replica_step_split(const ReplicaArgs a) {
+  pdl::wait_and_release();
   constexpr int CPW = 32 / G;  // columns per warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int grp = lane / CPW, col = lane - grp * CPW;
@@ -506,6 +509,7 @@ __global__ void __launch_bounds__(kMaxClasses * 32) softmax_logits_kernel(
     int j0, float* __restrict__ E) {
   extern __shared__ __align__(16) float xs[];  // [in_dim]
   __shared__ float lg[kMaxClasses];
+  pdl::wait_and_release();
   const int slot = blockIdx.x, t = blockIdx.y;
   __shared__ int row_sm;
   __shared__ __align__(8) uint64_t bar;
@@ -549,6 +553,7 @@ __global__ void __launch_bounds__(256) softmax_wgrad_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
     int classes, int j0, int64_t ld, const float* __restrict__ E, float* __restrict__ Gall) {
   extern __shared__ float sm[];
+  pdl::wait_and_release();
   float* xs = sm;                  // [b][kFeat]
   float* e = xs + b * kFeat;       // [b][classes]
   __shared__ int rows[64];
@@ -592,6 +597,7 @@ __global__ void __launch_bounds__(256) softmax_round_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
     int classes, int j0, const float* __restrict__ E, float* __restrict__ Gall, const ReplicaArgs a) {
   extern __shared__ float sm[];
+  pdl::wait_and_release();
   const int r = a.r;
   float* xs = sm;                              // [r][b][kFeatF]
   float* e = xs + (int64_t)r * b * kFeatF;     // [r][b][classes]
@@ -665,6 +671,11 @@ __global__ void __launch_bounds__(kThreads) broadcast_rows_kernel(float* __restr
 }
 
 template <typename K>
+cudaError_t launch_pdl(K kernel, int grid, cudaStream_t s, const ReplicaArgs& a) {
+  return pdl::launch(kernel, dim3(grid), dim3(kThreads), 0, s, 1, a);
+}
+
+template <typename K>
 int grid_for(K kernel, int threads, size_t smem, int64_t work_items, int num_sms) {
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess ||
@@ -722,15 +733,13 @@ cudaError_t launch_ldg_uj(const ReplicaArgs& a, int64_t work, int num_sms, cudaS
   if (UJ == 2 && ldg_minblocks() == 8) k = replica_step_ldg<MODE, 2, 8>;
   const int grid = ldg_full_grid() ? (int)((work + kThreads - 1) / kThreads)
                                    : grid_for(k, kThreads, 0, work, num_sms);
-  k<<<grid < 1 ? 1 : grid, kThreads, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(k, grid < 1 ? 1 : grid, s, a);
 }
 
 template <int MODE>
 cudaError_t launch_ldg_default(const ReplicaArgs& a, int64_t work, cudaStream_t s) {
   const int grid = (int)((work + kThreads - 1) / kThreads);
-  replica_step_ldg<MODE, 2><<<grid < 1 ? 1 : grid, kThreads, 0, s>>>(a);
-  return cudaGetLastError();
+  return launch_pdl(replica_step_ldg<MODE, 2>, grid < 1 ? 1 : grid, s, a);
 }
 
 template <int MODE>
@@ -768,12 +777,21 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
   const bool split = a.c0 == 0 && mode != kLocal && a.r >= 2 &&
                      (a.n4 < split_below / 4 || (a.n4 < split_below && a.r >= 8));
   if (split) {
-    const int G = a.r >= 4 ? 4 : 2;
+    static const int g_knob = [] {  // SMA_SPLIT_G = 2|4|8|16: experiments only
+      const char* e = getenv("SMA_SPLIT_G");
+      const int v = e ? atoi(e) : 0;
+      return (v == 2 || v == 4 || v == 8 || v == 16) ? v : 0;
+    }();
+    int G = a.r >= 4 ? 4 : 2;
+    if (g_knob) G = g_knob;
     const int64_t cols_per_block = (kThreads / 32) * (32 / G);
     const int grid = (int)((a.n4 + cols_per_block - 1) / cols_per_block);
 #define SMA_SPLIT_LAUNCH(M)                                                                  \
-  if (G == 4) replica_step_split<M, 4><<<grid, kThreads, 0, s>>>(a);                          \
-  else replica_step_split<M, 2><<<grid, kThreads, 0, s>>>(a);
+  if (G == 16) e = launch_pdl(replica_step_split<M, 16>, grid, s, a);                         \
+  else if (G == 8) e = launch_pdl(replica_step_split<M, 8>, grid, s, a);                      \
+  else if (G == 4) e = launch_pdl(replica_step_split<M, 4>, grid, s, a);                      \
+  else e = launch_pdl(replica_step_split<M, 2>, grid, s, a);
+    cudaError_t e = cudaSuccess;
     switch (mode) {
       case kFused: SMA_SPLIT_LAUNCH(kFused) break;
       case kPartialA: SMA_SPLIT_LAUNCH(kPartialA) break;
@@ -784,7 +802,7 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
       default: return cudaErrorInvalidValue;
     }
 #undef SMA_SPLIT_LAUNCH
-    return cudaGetLastError();
+    return e;
   }
   switch (mode) {
     case kFused: return launch_ldg<kFused>(a, work, num_sms, s);
@@ -864,11 +882,11 @@ cudaError_t launch_softmax_grad(const float* X, const int32_t* y, const int32_t*
   const size_t sm2 = sizeof(float) * ((size_t)b * kFeat + (size_t)b * classes);
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(softmax_logits_kernel), (int)sm1);
   if (e != cudaSuccess) return e;
-  softmax_logits_kernel<<<dim3(r, b), classes * 32, sm1, s>>>(X, y, perm, pos0, b, in_dim, classes, W,
-                                                              ld, j0, E);
-  softmax_wgrad_kernel<<<dim3(r, (in_dim + kFeat - 1) / kFeat), 256, sm2, s>>>(
-      X, perm, pos0, b, in_dim, classes, j0, ld, E, G);
-  return cudaGetLastError();
+  e = pdl::launch(softmax_logits_kernel, dim3(r, b), dim3(classes * 32), sm1, s, 1, X, y, perm, pos0,
+                  b, in_dim, classes, W, ld, j0, E);
+  if (e != cudaSuccess) return e;
+  return pdl::launch(softmax_wgrad_kernel, dim3(r, (in_dim + kFeat - 1) / kFeat), dim3(256), sm2, s,
+                     1, X, perm, pos0, b, in_dim, classes, j0, ld, E, G);
 }
 
 cudaError_t launch_softmax_round(const float* X, const int32_t* y, const int32_t* perm,
@@ -884,11 +902,12 @@ cudaError_t launch_softmax_round(const float* X, const int32_t* y, const int32_t
   if (e != cudaSuccess) return e;
   if ((e = ensure_dyn_smem(reinterpret_cast<const void*>(softmax_round_kernel), (int)sm2)) != cudaSuccess)
     return e;
-  softmax_logits_kernel<<<dim3(a.r, b), classes * 32, sm1, s>>>(X, y, perm, pos0, b, in_dim, classes,
-                                                                a.W, a.ld, j0, E);
+  e = pdl::launch(softmax_logits_kernel, dim3(a.r, b), dim3(classes * 32), sm1, s, 1, X, y, perm,
+                  pos0, b, in_dim, classes, (const float*)a.W, a.ld, j0, E);
+  if (e != cudaSuccess) return e;
   const int nfs = (in_dim + kFeatF - 1) / kFeatF;
-  softmax_round_kernel<<<nfs + 1, 256, sm2, s>>>(X, perm, pos0, b, in_dim, classes, j0, E, G, a);
-  return cudaGetLastError();
+  return pdl::launch(softmax_round_kernel, dim3(nfs + 1), dim3(256), sm2, s, 1, X, perm, pos0, b,
+                     in_dim, classes, j0, (const float*)E, G, a);
 }
 
 cudaError_t launch_broadcast_rows(float* dst, int64_t ld, int r, const float* src, int64_t n4,

@@ -19,6 +19,7 @@
 
 #include "sma_bulk.cuh"
 #include "sma_dot2.cuh"
+#include "sma_pdl.cuh"
 #include "sma_softmax.cuh"
 #include "sma_internal.h"
 
@@ -40,6 +41,7 @@ using dot2::f2_add;
 __global__ void __launch_bounds__(kMlpThreads) mlp_hidden_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
     int hidden, const float* __restrict__ Wall, int64_t ld, int j0, float2* __restrict__ A1) {
+  pdl::wait_and_release();
   // R18: the pre-activation that decides the ReLU mask is accumulated in
   // double-float (hi + lo), accurate to ~2^-48 like the oracle's fp64.
   extern __shared__ __align__(16) float sm[];
@@ -122,6 +124,7 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_logits_kernel(
     const int32_t* __restrict__ y, const int32_t* __restrict__ perm, int64_t pos0, int b,
     int in_dim, int hidden, int classes, const float* __restrict__ Wall, int64_t ld, int j0,
     const float2* __restrict__ A1, float* __restrict__ E) {
+  pdl::wait_and_release();
   extern __shared__ __align__(16) float sm[];
   float* hrow = sm;                 // [hidden]
   __shared__ float lg[32];
@@ -155,6 +158,7 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_head_kernel(
     int b, int in_dim, int hidden, int classes, const float* __restrict__ Wall, int64_t ld,
     const float2* __restrict__ A1, const float* __restrict__ E, float* __restrict__ DA,
     float* __restrict__ Gall) {
+  pdl::wait_and_release();
   extern __shared__ __align__(16) float sm[];
   float* hs = sm;                              // [b][hidden]
   float* w2s = hs + b * hidden;                // [classes][hidden]
@@ -206,6 +210,7 @@ constexpr int kFeat = 64;
 __global__ void __launch_bounds__(kMlpThreads) mlp_w1_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
     int hidden, int j0, int64_t ld, const float* __restrict__ DA, float* __restrict__ Gall) {
+  pdl::wait_and_release();
   extern __shared__ __align__(16) float sm[];
   float* xs = sm;                       // [b][kFeat]
   float* da = xs + b * kFeat;           // [b][kUnits]
@@ -261,18 +266,20 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
   // else the SIMT kernel; both write the same A1 contract
   e = launch_mlp_hidden_tc(X, perm, pos0, b, in_dim, hidden, W, ld, r, j0, A1, s);
   if (e == cudaErrorNotSupported)
-    mlp_hidden_kernel<<<g1, kMlpThreads, sm1, s>>>(X, perm, pos0, b, in_dim, hidden, W, ld, j0, A1);
-  else if (e != cudaSuccess)
+    e = pdl::launch(mlp_hidden_kernel, g1, dim3(kMlpThreads), sm1, s, 1, X, perm, pos0, b, in_dim,
+                    hidden, W, ld, j0, A1);
+  if (e != cudaSuccess) return e;
+  if ((e = pdl::launch(mlp_logits_kernel, gL, dim3(kMlpThreads), smL, s, 1, y, perm, pos0, b, in_dim,
+                       hidden, classes, W, ld, j0, (const float2*)A1, E)) != cudaSuccess)
     return e;
-  mlp_logits_kernel<<<gL, kMlpThreads, smL, s>>>(y, perm, pos0, b, in_dim, hidden, classes, W, ld,
-                                                 j0, A1, E);
-  mlp_head_kernel<<<g2, kMlpThreads, sm2, s>>>(b, in_dim, hidden, classes, W, ld, A1, E, DA, G);
+  if ((e = pdl::launch(mlp_head_kernel, g2, dim3(kMlpThreads), sm2, s, 1, b, in_dim, hidden, classes,
+                       W, ld, (const float2*)A1, (const float*)E, DA, G)) != cudaSuccess)
+    return e;
   e = launch_mlp_w1_tc(X, perm, pos0, b, in_dim, hidden, j0, ld, r, DA, G, s);
   if (e == cudaErrorNotSupported)
-    mlp_w1_kernel<<<g3, kMlpThreads, sm3, s>>>(X, perm, pos0, b, in_dim, hidden, j0, ld, DA, G);
-  else if (e != cudaSuccess)
-    return e;
-  return cudaGetLastError();
+    e = pdl::launch(mlp_w1_kernel, g3, dim3(kMlpThreads), sm3, s, 1, X, perm, pos0, b, in_dim, hidden,
+                    j0, ld, (const float*)DA, G);
+  return e;
 }
 
 }  // namespace sma

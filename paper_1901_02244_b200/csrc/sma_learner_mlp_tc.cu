@@ -41,6 +41,7 @@
 #include <mutex>
 
 #include "sma_dot2.cuh"
+#include "sma_pdl.cuh"
 #include "sma_internal.h"
 
 namespace sma {
@@ -141,6 +142,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_hidden_tc_kernel(
   const int nstep = (kb + 7) / 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  pdl::wait_and_release();  // W1 (the replica) and A1's readers come from the previous kernels
   // Prologue, overlapped: lane 0 of warp 1 initialises the barriers and issues
   // the TMA boxes at once; every thread starts its X loads (reading the batch
   // permutation itself); warp 0 allocates TMEM meanwhile.
@@ -368,6 +370,7 @@ __global__ void __launch_bounds__(kTcThreads) mlp_w1_tc_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t* prow = perm + pos0 + (int64_t)(j0 + slot) * b;
   const float* da = DA + (int64_t)slot * b * hidden;
+  pdl::wait_and_release();
 
   if (threadIdx.x == 32) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar_mma)));
@@ -548,20 +551,8 @@ cudaError_t launch_mlp_hidden_tc(const float* X, const int32_t* perm, int64_t po
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_hidden_tc_kernel), kSmemBytes);
   if (e != cudaSuccess) return e;
   const int nks = (in_dim + kTcKC - 1) / kTcKC;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nks, hidden / kTcM, r);
-  cfg.blockDim = dim3(kTcThreads);
-  cfg.dynamicSmemBytes = kSmemBytes;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = nks;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, mlp_hidden_tc_kernel, tm, X, perm, pos0, b, in_dim, hidden, W, ld,
-                            j0, A1);
+  return pdl::launch(mlp_hidden_tc_kernel, dim3(nks, hidden / kTcM, r), dim3(kTcThreads),
+                     (size_t)kSmemBytes, s, nks, tm, X, perm, pos0, b, in_dim, hidden, W, ld, j0, A1);
 }
 
 }  // namespace sma
@@ -579,7 +570,7 @@ cudaError_t launch_mlp_w1_tc(const float* X, const int32_t* perm, int64_t pos0, 
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_w1_tc_kernel), kW1Smem);
   if (e != cudaSuccess) return e;
   const dim3 grid((in_dim + kW1N - 1) / kW1N, hidden / kTcM, r);
-  mlp_w1_tc_kernel<<<grid, kTcThreads, kW1Smem, s>>>(X, perm, pos0, b, in_dim, hidden, j0, ld, DA, G);
-  return cudaGetLastError();
+  return pdl::launch(mlp_w1_tc_kernel, grid, dim3(kTcThreads), (size_t)kW1Smem, s, 1, X, perm, pos0, b,
+                     in_dim, hidden, j0, ld, DA, G);
 }
 }  // namespace sma
