@@ -167,6 +167,9 @@ cudaError_t launch_zsync_p2p(int mode, const P2PArgs& a, int num_ctas, cudaStrea
   const int64_t want = (a.len4 + kP2PThreads - 1) / kP2PThreads;
   int grid = (int)((num_ctas > 0 && want > num_ctas) ? num_ctas : want);
   if (grid < 1) grid = 1;
+  // Launched without PDL (no measurable gain on one GPU: C3 Mode A 41-46k rounds/s
+  // either way, within the run-to-run spread of the barrier spin; profiles/r01_pdl.txt),
+  // so the next replica kernel starts only after this kernel has completed.
   if (mode == kPartialA)
     zsync_p2p_kernel<kPartialA><<<grid, kP2PThreads, 0, s>>>(a);
   else
