@@ -27,6 +27,7 @@ namespace sma {
 namespace {
 constexpr int kUnits = 16;       // hidden units per CTA of the dW1 kernel
 constexpr int kHidUnits = 4;     // hidden units per CTA of the forward kernel
+constexpr int kRowBatch = 8;     // batch rows per warp of the forward kernel (independent chains)
 constexpr int kMlpThreads = 256;
 constexpr int kHeadSplit = 16;   // CTAs per learner of the head-gradient kernel
 
@@ -38,7 +39,7 @@ using dot2::f2;
 using dot2::dot2_step;
 using dot2::f2_add;
 
-__global__ void __launch_bounds__(kMlpThreads) mlp_hidden_kernel(
+__global__ void __launch_bounds__(kMlpThreads, 1) mlp_hidden_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
     int hidden, const float* __restrict__ Wall, int64_t ld, int j0, float2* __restrict__ A1) {
   pdl::wait_and_release();
@@ -59,61 +60,86 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_hidden_kernel(
   bulk::stage_rows_span(xs, X, rows, b, in_dim, in_dim, 0, ws, W1 + (int64_t)k0 * in_dim,
                         nu * in_dim, &bar, 0, true);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int pr = warp; pr < b * nu; pr += nw) {
-    const int t = pr / nu, u = pr - t * nu;
+  // Each warp takes one hidden unit u and a group of kRowBatch batch rows: the W1
+  // row chunk is loaded once per lane iteration and reused for every row, and
+  // the rows' accumulators are independent FMA chains (the per-row arithmetic,
+  // lane-strided over f with 4 components per float4, is unchanged).
+  const int ngrp = (b + kRowBatch - 1) / kRowBatch;
+  for (int pr = warp; pr < nu * ngrp; pr += nw) {
+    const int u = pr % nu, t0 = (pr / nu) * kRowBatch;
+    const int nt = min(kRowBatch, b - t0);
     const float* w = ws + (int64_t)u * in_dim;
-    const float* x = xs + (int64_t)t * in_dim;
     // fast path: plain fp32 dot and sum_f |w x|; the fp32 result's sign is
     // certain unless |a| <= 2^-12 sum|w x| (> 3x the n u sum|w x| error bound
     // for n <= 1024), and only then (rare; warp-uniform) is the dot redone
     // with the Dot2 accumulation.
-    float sv = 0.f, sa = 0.f;
+    float sv[kRowBatch], sa[kRowBatch];
+#pragma unroll
+    for (int i = 0; i < kRowBatch; ++i) sv[i] = sa[i] = 0.f;
     if ((in_dim & 3) == 0) {  // 128-bit shared-memory loads: half the instructions
       const float4* w4 = reinterpret_cast<const float4*>(w);
-      const float4* x4 = reinterpret_cast<const float4*>(x);
       for (int f = lane; f < (in_dim >> 2); f += 32) {
-        const float4 p = w4[f], q = x4[f];
-        sv = __fmaf_rn(p.x, q.x, sv);
-        sv = __fmaf_rn(p.y, q.y, sv);
-        sv = __fmaf_rn(p.z, q.z, sv);
-        sv = __fmaf_rn(p.w, q.w, sv);
-        sa = __fmaf_rn(fabsf(p.x), fabsf(q.x), sa);
-        sa = __fmaf_rn(fabsf(p.y), fabsf(q.y), sa);
-        sa = __fmaf_rn(fabsf(p.z), fabsf(q.z), sa);
-        sa = __fmaf_rn(fabsf(p.w), fabsf(q.w), sa);
+        const float4 p = w4[f];
+#pragma unroll
+        for (int i = 0; i < kRowBatch; ++i) {
+          if (i < nt) {
+            const float4 q = reinterpret_cast<const float4*>(xs + (int64_t)(t0 + i) * in_dim)[f];
+            sv[i] = __fmaf_rn(p.x, q.x, sv[i]);
+            sv[i] = __fmaf_rn(p.y, q.y, sv[i]);
+            sv[i] = __fmaf_rn(p.z, q.z, sv[i]);
+            sv[i] = __fmaf_rn(p.w, q.w, sv[i]);
+            sa[i] = __fmaf_rn(fabsf(p.x), fabsf(q.x), sa[i]);
+            sa[i] = __fmaf_rn(fabsf(p.y), fabsf(q.y), sa[i]);
+            sa[i] = __fmaf_rn(fabsf(p.z), fabsf(q.z), sa[i]);
+            sa[i] = __fmaf_rn(fabsf(p.w), fabsf(q.w), sa[i]);
+          }
+        }
       }
     } else {
       for (int f = lane; f < in_dim; f += 32) {
-        sv = __fmaf_rn(w[f], x[f], sv);
-        sa = __fmaf_rn(fabsf(w[f]), fabsf(x[f]), sa);
-      }
-    }
 #pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      sv = __fadd_rn(sv, __shfl_xor_sync(0xffffffffu, sv, off));
-      sa = __fadd_rn(sa, __shfl_xor_sync(0xffffffffu, sa, off));
+        for (int i = 0; i < kRowBatch; ++i) {
+          if (i < nt) {
+            const float q = xs[(int64_t)(t0 + i) * in_dim + f];
+            sv[i] = __fmaf_rn(w[f], q, sv[i]);
+            sa[i] = __fmaf_rn(fabsf(w[f]), fabsf(q), sa[i]);
+          }
+        }
+      }
     }
     const float bias = b1[k0 + u];
-    f2 acc = {__fadd_rn(sv, bias), 0.f};
-    const float bound = ldexpf(__fadd_rn(sa, fabsf(bias)), -12);
-    if (fabsf(acc.hi) <= bound) {  // near a ReLU kink: decide at ~2^-48
-      acc = f2{0.f, 0.f};
-      if ((in_dim & 3) == 0) {
-        const float4* w4 = reinterpret_cast<const float4*>(w);
-        const float4* x4 = reinterpret_cast<const float4*>(x);
-        for (int f = lane; f < (in_dim >> 2); f += 32) {
-          const float4 a = w4[f], c = x4[f];
-          dot2_step(acc, a.x, c.x);
-          dot2_step(acc, a.y, c.y);
-          dot2_step(acc, a.z, c.z);
-          dot2_step(acc, a.w, c.w);
-        }
-      } else {
-        for (int f = lane; f < in_dim; f += 32) dot2_step(acc, w[f], x[f]);
+#pragma unroll
+    for (int i = 0; i < kRowBatch; ++i) {
+      if (i >= nt) break;
+      float v = sv[i], va = sa[i];
+#pragma unroll
+      for (int off = 16; off >= 1; off >>= 1) {
+        v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, off));
+        va = __fadd_rn(va, __shfl_xor_sync(0xffffffffu, va, off));
       }
-      acc = f2_add(dot2::warp_sum(acc), f2{bias, 0.f});
+      const int t = t0 + i;
+      const float* x = xs + (int64_t)t * in_dim;
+      f2 acc = {__fadd_rn(v, bias), 0.f};
+      const float bound = ldexpf(__fadd_rn(va, fabsf(bias)), -12);
+      if (fabsf(acc.hi) <= bound) {  // near a ReLU kink: decide at ~2^-48 (warp-uniform)
+        acc = f2{0.f, 0.f};
+        if ((in_dim & 3) == 0) {
+          const float4* w4 = reinterpret_cast<const float4*>(w);
+          const float4* x4 = reinterpret_cast<const float4*>(x);
+          for (int f = lane; f < (in_dim >> 2); f += 32) {
+            const float4 a = w4[f], c = x4[f];
+            dot2_step(acc, a.x, c.x);
+            dot2_step(acc, a.y, c.y);
+            dot2_step(acc, a.z, c.z);
+            dot2_step(acc, a.w, c.w);
+          }
+        } else {
+          for (int f = lane; f < in_dim; f += 32) dot2_step(acc, w[f], x[f]);
+        }
+        acc = f2_add(dot2::warp_sum(acc), f2{bias, 0.f});
+      }
+      if (lane == 0) A1[((int64_t)slot * b + t) * hidden + k0 + u] = make_float2(acc.hi, acc.lo);
     }
-    if (lane == 0) A1[((int64_t)slot * b + t) * hidden + k0 + u] = make_float2(acc.hi, acc.lo);
   }
 }
 

@@ -491,10 +491,11 @@ EncodeTiledFn g_encode = nullptr;
 std::once_flag g_encode_once;
 
 // SMA_MLP_TC: 0 = SIMT kernels, 1 = tensor cores, unset = by learners per GPU:
-// measured (profiles/r01_mlp_tc_sweep.txt, MLP rounds/s, b = 16) the two
-// tensor-core GEMMs (layer 1 + dW1) are 14-22 % slower at r <= 4 (56 CTAs of
-// short latency phases vs the SIMT kernels' 256-832), even at r = 6, and
-// 4 / 10 / 22 / 26 % faster at r = 8 / 12 / 16 / 32.
+// measured (profiles/r01_mlp_tc_sweep.txt, MLP rounds/s, b = 16, PDL on) the two
+// tensor-core GEMMs (layer 1 + dW1) lose while the SIMT kernels' many small CTAs
+// still fit the GPU (k = 4: 32.1k SIMT vs 25.8k; k = 8: 21.9k vs 20.5k; 56 CTAs of
+// short latency phases) and win from r = 10 on (19.8k vs 17.9k; r = 16: 16.0k
+// vs 13.4k).
 int tc_policy() {
   static const int p = [] {
     const char* e = getenv("SMA_MLP_TC");
@@ -511,7 +512,7 @@ cudaError_t launch_mlp_hidden_tc(const float* X, const int32_t* perm, int64_t po
                                  int in_dim, int hidden, const float* W, int64_t ld, int r, int j0,
                                  float2* A1, cudaStream_t s) {
   const int pol = tc_policy();
-  if (pol == 0 || (pol < 0 && r < 8) || b > kTcN || b < 1 || hidden % kTcM != 0 || hidden > 65535 ||
+  if (pol == 0 || (pol < 0 && r < 10) || b > kTcN || b < 1 || hidden % kTcM != 0 || hidden > 65535 ||
       (in_dim & 3) != 0 || in_dim > kMaxCluster * kTcKC || r < 1)
     return cudaErrorNotSupported;
   std::call_once(g_encode_once, [] {
@@ -564,7 +565,7 @@ cudaError_t launch_mlp_w1_tc(const float* X, const int32_t* perm, int64_t pos0, 
                              int hidden, int j0, int64_t ld, int r, const float* DA, float* G,
                              cudaStream_t s) {
   const int pol = tc_policy();
-  if (pol == 0 || (pol < 0 && r < 8) || b < 1 || b > kBoxK || hidden % kTcM != 0 ||
+  if (pol == 0 || (pol < 0 && r < 10) || b < 1 || b > kBoxK || hidden % kTcM != 0 ||
       (in_dim & 3) != 0 || r < 1)
     return cudaErrorNotSupported;
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_w1_tc_kernel), kW1Smem);
