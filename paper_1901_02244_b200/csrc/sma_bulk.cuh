@@ -55,8 +55,10 @@ __device__ __forceinline__ void wait(uint64_t* bar, uint32_t parity) {
 //   span:  n_span contiguous floats src_span -> dst_span (n_span may be 0).
 // `bar` is a shared mbarrier used once per call; pass init = true on its first
 // use and alternate `phase` (0, 1, 0, ...) on later ones.  Falls back to a
-// cooperative copy when a span is not 16-byte aligned / sized.
-__device__ __forceinline__ void stage_rows_span(float* dst_rows, const float* src, const int* row_idx,
+// cooperative copy when a span is not 16-byte aligned / sized.  Returns whether
+// the barrier was used (uniform across the CTA), so a caller staging twice
+// knows the next call's phase / init.
+__device__ __forceinline__ bool stage_rows_span(float* dst_rows, const float* src, const int* row_idx,
                                                 int nrows, int row_floats, int64_t stride, int col,
                                                 float* dst_span, const float* src_span, int n_span,
                                                 uint64_t* bar, uint32_t phase, bool init) {
@@ -74,6 +76,7 @@ __device__ __forceinline__ void stage_rows_span(float* dst_rows, const float* sr
     }
     __syncthreads();
     wait(bar, phase);
+    return true;
   } else {
     for (int q = threadIdx.x; q < nrows * row_floats; q += blockDim.x) {
       const int t = q / row_floats, f = q - t * row_floats;
@@ -81,6 +84,7 @@ __device__ __forceinline__ void stage_rows_span(float* dst_rows, const float* sr
     }
     for (int q = threadIdx.x; q < n_span; q += blockDim.x) dst_span[q] = src_span[q];
     __syncthreads();
+    return false;
   }
 }
 

@@ -509,7 +509,6 @@ __global__ void __launch_bounds__(kMaxClasses * 32) softmax_logits_kernel(
     int j0, float* __restrict__ E) {
   extern __shared__ __align__(16) float xs[];  // [in_dim]
   __shared__ float lg[kMaxClasses];
-  pdl::wait_and_release();
   const int slot = blockIdx.x, t = blockIdx.y;
   __shared__ int row_sm;
   __shared__ __align__(8) uint64_t bar;
@@ -521,6 +520,9 @@ __global__ void __launch_bounds__(kMaxClasses * 32) softmax_logits_kernel(
   const float* W = Wall + (int64_t)slot * ld;
   const bool vec = (in_dim & 3) == 0 && ((reinterpret_cast<uintptr_t>(X) & 15) == 0);
   bulk::stage_rows_span(xs, X, &row_sm, 1, in_dim, in_dim, 0, nullptr, nullptr, 0, &bar, 0, true);
+  // PDL: the batch row (X, perm, y: never written by a kernel) is staged while
+  // the previous kernel drains; the replica W is read only after the wait
+  pdl::wait_and_release();
   const int lane = threadIdx.x & 31, c = threadIdx.x >> 5;
   if (c < classes) {  // warp c: logit of class c, W row c read straight from L2
     const float* w = W + (int64_t)c * in_dim;
@@ -553,7 +555,6 @@ __global__ void __launch_bounds__(256) softmax_wgrad_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
     int classes, int j0, int64_t ld, const float* __restrict__ E, float* __restrict__ Gall) {
   extern __shared__ float sm[];
-  pdl::wait_and_release();
   float* xs = sm;                  // [b][kFeat]
   float* e = xs + b * kFeat;       // [b][classes]
   __shared__ int rows[64];
@@ -562,10 +563,13 @@ __global__ void __launch_bounds__(256) softmax_wgrad_kernel(
   float* G = Gall + (int64_t)slot * ld;
   __shared__ __align__(8) uint64_t bar;
   if (threadIdx.x < b) rows[threadIdx.x] = perm[pos0 + (int64_t)(j0 + slot) * b + threadIdx.x];
+  __syncthreads();
+  // X[rows][f0, f0 + nf) -> xs [b][nf] in one TMA bulk transaction, while the
+  // logits kernel drains (PDL); E (its output) only after the wait
+  bulk::stage_rows_span(xs, X, rows, b, nf, in_dim, f0, nullptr, nullptr, 0, &bar, 0, true);
+  pdl::wait_and_release();
   for (int q = threadIdx.x; q < b * classes; q += blockDim.x) e[q] = E[(int64_t)slot * b * classes + q];
   __syncthreads();
-  // X[rows][f0, f0 + nf) -> xs [b][nf] in one TMA bulk transaction
-  bulk::stage_rows_span(xs, X, rows, b, nf, in_dim, f0, nullptr, nullptr, 0, &bar, 0, true);
   const float fb = (float)b;
   for (int q = threadIdx.x; q < classes * nf; q += blockDim.x) {
     const int c = q / nf, f = q - c * nf;

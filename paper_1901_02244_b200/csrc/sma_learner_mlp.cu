@@ -42,7 +42,6 @@ using dot2::f2_add;
 __global__ void __launch_bounds__(kMlpThreads, 1) mlp_hidden_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
     int hidden, const float* __restrict__ Wall, int64_t ld, int j0, float2* __restrict__ A1) {
-  pdl::wait_and_release();
   // R18: the pre-activation that decides the ReLU mask is accumulated in
   // double-float (hi + lo), accurate to ~2^-48 like the oracle's fp64.
   extern __shared__ __align__(16) float sm[];
@@ -56,9 +55,13 @@ __global__ void __launch_bounds__(kMlpThreads, 1) mlp_hidden_kernel(
   __shared__ __align__(8) uint64_t bar;
   if (threadIdx.x < b) rows[threadIdx.x] = batch_row(perm, pos0, j0 + slot, b, threadIdx.x);
   __syncthreads();
-  // the batch rows and this CTA's W1 rows in one TMA bulk transaction
-  bulk::stage_rows_span(xs, X, rows, b, in_dim, in_dim, 0, ws, W1 + (int64_t)k0 * in_dim,
-                        nu * in_dim, &bar, 0, true);
+  // the batch rows (X, perm: never written by a kernel) while the previous
+  // kernel drains (PDL), then -- after the wait -- this CTA's W1 rows (the replica)
+  const bool used = bulk::stage_rows_span(xs, X, rows, b, in_dim, in_dim, 0, nullptr, nullptr, 0,
+                                          &bar, 0, true);
+  pdl::wait_and_release();
+  bulk::stage_rows_span(nullptr, X, rows, 0, in_dim, in_dim, 0, ws, W1 + (int64_t)k0 * in_dim,
+                        nu * in_dim, &bar, used ? 1u : 0u, !used);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   // Each warp takes one hidden unit u and a group of kRowBatch batch rows: the W1
   // row chunk is loaded once per lane iteration and reused for every row, and
@@ -236,7 +239,6 @@ constexpr int kFeat = 64;
 __global__ void __launch_bounds__(kMlpThreads) mlp_w1_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
     int hidden, int j0, int64_t ld, const float* __restrict__ DA, float* __restrict__ Gall) {
-  pdl::wait_and_release();
   extern __shared__ __align__(16) float sm[];
   float* xs = sm;                       // [b][kFeat]
   float* da = xs + b * kFeat;           // [b][kUnits]
@@ -248,13 +250,15 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_w1_kernel(
   const int nu = min(kUnits, hidden - k0);
   if (threadIdx.x < b) rows[threadIdx.x] = batch_row(perm, pos0, j0 + slot, b, threadIdx.x);
   __syncthreads();
-  // da1[t][k0, k0 + nu) -> da [b][nu] with plain loads (in flight while) the
-  // X[rows][f0, f0 + nf) -> xs [b][nf] TMA bulk transaction completes
+  // X[rows][f0, f0 + nf) -> xs [b][nf] (one TMA bulk transaction) while the head
+  // kernel drains (PDL); then da1[t][k0, k0 + nu) -> da [b][nu], its output
+  bulk::stage_rows_span(xs, X, rows, b, nf, in_dim, f0, nullptr, nullptr, 0, &bar, 0, true);
+  pdl::wait_and_release();
   for (int q = threadIdx.x; q < b * nu; q += blockDim.x) {
     const int t = q / nu, u = q - t * nu;
     da[q] = DA[((int64_t)slot * b + t) * hidden + k0 + u];
   }
-  bulk::stage_rows_span(xs, X, rows, b, nf, in_dim, f0, nullptr, nullptr, 0, &bar, 0, true);
+  __syncthreads();
   const float fb = (float)b;
   for (int q = threadIdx.x; q < nu * nf; q += blockDim.x) {  // dW1 = da^T x / b
     const int u = q / nf, f = q - u * nf;

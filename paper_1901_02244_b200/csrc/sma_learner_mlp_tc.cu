@@ -142,10 +142,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) mlp_hidden_tc_kernel(
   const int nstep = (kb + 7) / 8;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-  pdl::wait_and_release();  // W1 (the replica) and A1's readers come from the previous kernels
-  // Prologue, overlapped: lane 0 of warp 1 initialises the barriers and issues
-  // the TMA boxes at once; every thread starts its X loads (reading the batch
+  // PDL: wait for the previous kernel first (W1 is the replica it wrote; moving
+  // the X loads before the wait measured ~3 % slower at k = 16).  Prologue,
+  // overlapped: lane 0 of warp 1 initialises the barriers and issues the TMA
+  // boxes of W1 at once; every thread starts its X loads (reading the batch
   // permutation itself); warp 0 allocates TMEM meanwhile.
+  pdl::wait_and_release();
   if (threadIdx.x == 32) {  // 1. the W1 tile: nbox TMA boxes of 128 rows x 32 fp32
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar_tma)));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar_mma)));
@@ -370,7 +372,6 @@ __global__ void __launch_bounds__(kTcThreads) mlp_w1_tc_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int32_t* prow = perm + pos0 + (int64_t)(j0 + slot) * b;
   const float* da = DA + (int64_t)slot * b * hidden;
-  pdl::wait_and_release();
 
   if (threadIdx.x == 32) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar_mma)));
@@ -385,12 +386,16 @@ __global__ void __launch_bounds__(kTcThreads) mlp_w1_tc_kernel(
   // thread issues all of its loads before the first use (one memory latency)
   constexpr int kAE = kTcM * kBoxK / kTcThreads, kBE = kW1N * kBoxK / kTcThreads;
   static_assert(kAE * kTcThreads == kTcM * kBoxK && kBE * kTcThreads == kW1N * kBoxK, "tiling");
+  // all loads after the PDL wait, in flight together (da1 is the head kernel's
+  // output; issuing the X loads before the wait measured slower: a second
+  // serialised latency once the head kernel has already completed)
+  pdl::wait_and_release();
   float av[kAE], bv[kBE];
 #pragma unroll
   for (int i = 0; i < kAE; ++i) {
     const int e = threadIdx.x + i * kTcThreads;
     const int t = e / kTcM, u = e - t * kTcM;
-    av[i] = t < b ? __ldg(da + (int64_t)t * hidden + u0 + u) : 0.f;
+    av[i] = t < b ? da[(int64_t)t * hidden + u0 + u] : 0.f;
   }
 #pragma unroll
   for (int i = 0; i < kBE; ++i) {
