@@ -21,6 +21,7 @@
 
 #include <cmath>
 #include <functional>
+#include <future>
 #include <string>
 #include <vector>
 
@@ -131,7 +132,13 @@ struct sma_handle {
   uint64_t batch_seed = 0;
   int32_t* perm_dev[2] = {nullptr, nullptr};
   int64_t perm_epoch[2] = {-1, -1};
-  int32_t* perm_host = nullptr;
+  int32_t* perm_host[2] = {nullptr, nullptr};  // pinned staging, one per device buffer
+  cudaEvent_t perm_ev[2] = {nullptr, nullptr};  // the upload from perm_host[i] completed
+  bool perm_ev_used[2] = {false, false};
+  // the next epoch's permutation, computed on a host worker thread while the
+  // current epoch's rounds run (into perm_host[(e + 1) & 1])
+  std::future<void> perm_next;
+  int64_t perm_next_epoch = -1;
 
   float* z() const { return zbuf + (int64_t)cur * d_pad; }
   float* zprev() const { return zbuf + (int64_t)(1 - cur) * d_pad; }
@@ -214,7 +221,11 @@ void free_all(sma_handle* h) {
   cudaFree(h->mlp_A1);
   cudaFree(h->mlp_DA);
   cudaFree(h->mlp_E);
-  if (h->perm_host) cudaFreeHost(h->perm_host);
+  if (h->perm_next.valid()) h->perm_next.wait();
+  for (int i = 0; i < 2; ++i) {
+    if (h->perm_host[i]) cudaFreeHost(h->perm_host[i]);
+    if (h->perm_ev[i]) cudaEventDestroy(h->perm_ev[i]);
+  }
   delete h;
 }
 
@@ -1009,9 +1020,15 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
     h->perm_epoch[i] = -1;
     CUDA_TRY(cudaMalloc(&h->perm_dev[i], sizeof(int32_t) * (size_t)n_samples));
   }
-  if (h->perm_host) cudaFreeHost(h->perm_host);
-  h->perm_host = nullptr;
-  CUDA_TRY(cudaMallocHost(&h->perm_host, sizeof(int32_t) * (size_t)n_samples));
+  if (h->perm_next.valid()) h->perm_next.wait();
+  h->perm_next_epoch = -1;
+  for (int i = 0; i < 2; ++i) {
+    if (h->perm_host[i]) cudaFreeHost(h->perm_host[i]);
+    h->perm_host[i] = nullptr;
+    CUDA_TRY(cudaMallocHost(&h->perm_host[i], sizeof(int32_t) * (size_t)n_samples));
+    if (!h->perm_ev[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->perm_ev[i], cudaEventDisableTiming));
+    h->perm_ev_used[i] = false;
+  }
   STATUS_TRY(ensure_G(h));
   {  // learner scratch, sized for SMA_MAX_LOCAL_REPLICAS learners (resize-safe)
     cudaFree(h->mlp_A1);
@@ -1041,19 +1058,40 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
 }
 
 // The batch permutation of `round`'s epoch on the device (R10): built on the
-// host and uploaded when the epoch changes (double-buffered by epoch parity).
+// host and uploaded when the epoch changes, double-buffered by epoch parity on
+// both sides, with no host synchronisation of the stream: the upload is
+// stream-ordered after every earlier round of the handle (so after the last
+// kernel that read this device buffer, two epochs ago), and the host only waits
+// for the previous upload out of the same pinned buffer.
 static sma_status learner_batch(sma_handle* h, int64_t round, cudaStream_t s, int* buf_out,
                          int64_t* pos0_out) {
   const int64_t E = h->n_samples / ((int64_t)h->cfg.k * h->batch);
   const int64_t e = round / E;
   const int buf = (int)(e & 1);
   if (h->perm_epoch[buf] != e) {
-    STATUS_TRY(sync_handle(h));
-    plan_epoch_permutation(h->n_samples, h->batch_seed, e, h->perm_host);
-    CUDA_TRY(cudaMemcpyAsync(h->perm_dev[buf], h->perm_host, sizeof(int32_t) * h->n_samples,
+    if (h->perm_next.valid()) h->perm_next.wait();   // a prefetch may target this buffer
+    if (h->perm_next_epoch != e) {                   // not prefetched: build it now
+      if (h->perm_ev_used[buf]) CUDA_TRY(cudaEventSynchronize(h->perm_ev[buf]));
+      plan_epoch_permutation(h->n_samples, h->batch_seed, e, h->perm_host[buf]);
+    }
+    if (h->any_work) CUDA_TRY(cudaStreamWaitEvent(s, h->evDone, 0));
+    CUDA_TRY(cudaMemcpyAsync(h->perm_dev[buf], h->perm_host[buf], sizeof(int32_t) * h->n_samples,
                              cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaStreamSynchronize(s));
+    CUDA_TRY(cudaEventRecord(h->perm_ev[buf], s));
+    h->perm_ev_used[buf] = true;
     h->perm_epoch[buf] = e;
+    // prefetch epoch e + 1 on a host worker: it first waits for the upload of
+    // epoch e - 1 out of the same pinned buffer, then overwrites it
+    const int nb = buf ^ 1;
+    int32_t* dst = h->perm_host[nb];
+    cudaEvent_t prev = h->perm_ev_used[nb] ? h->perm_ev[nb] : nullptr;
+    const int64_t N = h->n_samples;
+    const uint64_t seed = h->batch_seed;
+    h->perm_next_epoch = e + 1;
+    h->perm_next = std::async(std::launch::async, [=] {
+      if (prev) cudaEventSynchronize(prev);
+      plan_epoch_permutation(N, seed, e + 1, dst);
+    });
   }
   *buf_out = buf;
   *pos0_out = (round % E) * h->cfg.k * (int64_t)h->batch;
