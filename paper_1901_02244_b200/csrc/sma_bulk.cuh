@@ -88,5 +88,30 @@ __device__ __forceinline__ bool stage_rows_span(float* dst_rows, const float* sr
   }
 }
 
+// Stage a [nrows][nf] tile of rows row_idx[t] (shared memory), columns
+// [col, col + nf), of a row-major matrix with `stride` floats per row into
+// dst [nrows][nf], by the whole CTA with one 16-byte load per thread and
+// element group (no synchronisation inside; the caller syncs).  For narrow
+// tiles this beats one TMA bulk copy per short row issued by a single thread
+// (MLP dW1: 16 rows x 256 B per CTA).  Scalar fallback when not 16-byte aligned.
+__device__ __forceinline__ void load_tile(float* dst, const float* src, const int* row_idx,
+                                          int nrows, int nf, int64_t stride, int col) {
+  const bool vec = ((nf | col) & 3) == 0 && ((stride & 3) == 0) &&
+                   ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) == 0;
+  if (vec) {
+    const int n4 = nf >> 2;
+    for (int q = threadIdx.x; q < nrows * n4; q += blockDim.x) {
+      const int t = q / n4, c = q - t * n4;
+      reinterpret_cast<float4*>(dst)[q] =
+          __ldg(reinterpret_cast<const float4*>(src + (int64_t)row_idx[t] * stride + col) + c);
+    }
+  } else {
+    for (int q = threadIdx.x; q < nrows * nf; q += blockDim.x) {
+      const int t = q / nf, f = q - t * nf;
+      dst[q] = __ldg(src + (int64_t)row_idx[t] * stride + col + f);
+    }
+  }
+}
+
 }  // namespace bulk
 }  // namespace sma

@@ -561,12 +561,11 @@ __global__ void __launch_bounds__(256) softmax_wgrad_kernel(
   const int slot = blockIdx.x, f0 = blockIdx.y * kFeat;
   const int nf = min(kFeat, in_dim - f0);
   float* G = Gall + (int64_t)slot * ld;
-  __shared__ __align__(8) uint64_t bar;
   if (threadIdx.x < b) rows[threadIdx.x] = perm[pos0 + (int64_t)(j0 + slot) * b + threadIdx.x];
   __syncthreads();
-  // X[rows][f0, f0 + nf) -> xs [b][nf] in one TMA bulk transaction, while the
+  // X[rows][f0, f0 + nf) -> xs [b][nf] (one 16-byte load per thread), while the
   // logits kernel drains (PDL); E (its output) only after the wait
-  bulk::stage_rows_span(xs, X, rows, b, nf, in_dim, f0, nullptr, nullptr, 0, &bar, 0, true);
+  bulk::load_tile(xs, X, rows, b, nf, in_dim, f0);
   pdl::wait_and_release();
   for (int q = threadIdx.x; q < b * classes; q += blockDim.x) e[q] = E[(int64_t)slot * b * classes + q];
   __syncthreads();

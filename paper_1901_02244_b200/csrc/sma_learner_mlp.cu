@@ -246,13 +246,13 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_w1_kernel(
   const int slot = blockIdx.x, k0 = blockIdx.y * kUnits, f0 = blockIdx.z * kFeat;
   const int nf = min(kFeat, in_dim - f0);
   float* G = Gall + (int64_t)slot * ld;
-  __shared__ __align__(8) uint64_t bar;
   const int nu = min(kUnits, hidden - k0);
   if (threadIdx.x < b) rows[threadIdx.x] = batch_row(perm, pos0, j0 + slot, b, threadIdx.x);
   __syncthreads();
-  // X[rows][f0, f0 + nf) -> xs [b][nf] (one TMA bulk transaction) while the head
-  // kernel drains (PDL); then da1[t][k0, k0 + nu) -> da [b][nu], its output
-  bulk::stage_rows_span(xs, X, rows, b, nf, in_dim, f0, nullptr, nullptr, 0, &bar, 0, true);
+  // X[rows][f0, f0 + nf) -> xs [b][nf] (one 16-byte load per thread: 16 short
+  // rows as TMA bulk copies from one thread were slower) while the head kernel
+  // drains (PDL); then da1[t][k0, k0 + nu) -> da [b][nu], its output
+  bulk::load_tile(xs, X, rows, b, nf, in_dim, f0);
   pdl::wait_and_release();
   for (int q = threadIdx.x; q < b * nu; q += blockDim.x) {
     const int t = q / nu, u = q - t * nu;
