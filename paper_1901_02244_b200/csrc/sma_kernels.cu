@@ -785,7 +785,11 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
       const int v = e ? atoi(e) : 0;
       return (v == 2 || v == 4 || v == 8 || v == 16) ? v : 0;
     }();
-    int G = a.r >= 4 ? 4 : 2;
+    // lanes per column: 2 once two lanes per column already give ~100k threads
+    // and r <= 16 (more replicas per lane in flight), else 4 (more parallelism);
+    // measured with PDL (profiles/r01_split.jsonl): C2 153k -> 169k rounds/s, C3
+    // 98k -> 102k with G = 2; C1 (d = 8k) and r = 32 are better with G = 4
+    int G = (a.n4 * 2 >= 100000 && a.r <= 16) ? 2 : (a.r >= 4 ? 4 : 2);
     if (g_knob) G = g_knob;
     const int64_t cols_per_block = (kThreads / 32) * (32 / G);
     const int grid = (int)((a.n4 + cols_per_block - 1) / cols_per_block);
