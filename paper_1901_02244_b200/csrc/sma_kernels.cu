@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) replica_step_ldg(const R
 // j = g, g + G, ... (two per load batch), and the G partial sums are combined
 // with log2(G) xor-shuffles (bitwise identical in every lane: fp addition is
 // commutative); group 0 finishes the column.  4x the threads for the same d.
-template <int MODE, int G>
+template <int MODE, int G, int UJ = 2>
 __global__ void __launch_bounds__(kThreads) replica_step_split(const ReplicaArgs a) {
   pdl::wait_and_release();
   constexpr int CPW = 32 / G;  // columns per warp
@@ -286,18 +286,20 @@ __global__ void __launch_bounds__(kThreads) replica_step_split(const ReplicaArgs
   bool bad = false;
   if (valid) {
     int j = grp;
-    for (; j + G < a.r; j += 2 * G) {
-      float4 w0 = ld_rw(a.W + (int64_t)j * a.ld + p0);
-      float4 w1 = ld_rw(a.W + (int64_t)(j + G) * a.ld + p0);
-      const float4 g0 = full ? ld_ro(a.g.p[j] + p0) : ld_tail(a.g.p[j], p0, a.d);
-      const float4 g1 = full ? ld_ro(a.g.p[j + G] + p0) : ld_tail(a.g.p[j + G], p0, a.d);
-      replica_update4<MODE>(w0, g0, z, acc, c4, a.alpha, a.gamma);
-      st4(a.W + (int64_t)j * a.ld + p0, w0);
-      if (matc) st4(a.C + (int64_t)j * a.ld + p0, c4);
-      replica_update4<MODE>(w1, g1, z, acc, c4, a.alpha, a.gamma);
-      st4(a.W + (int64_t)(j + G) * a.ld + p0, w1);
-      if (matc) st4(a.C + (int64_t)(j + G) * a.ld + p0, c4);
-      bad |= !finite4(w0) || !finite4(w1);
+    for (; j + (UJ - 1) * G < a.r; j += UJ * G) {  // UJ replicas of this lane in flight
+      float4 w[UJ], g[UJ];
+#pragma unroll
+      for (int u = 0; u < UJ; ++u) w[u] = ld_rw(a.W + (int64_t)(j + u * G) * a.ld + p0);
+#pragma unroll
+      for (int u = 0; u < UJ; ++u)
+        g[u] = full ? ld_ro(a.g.p[j + u * G] + p0) : ld_tail(a.g.p[j + u * G], p0, a.d);
+#pragma unroll
+      for (int u = 0; u < UJ; ++u) {
+        replica_update4<MODE>(w[u], g[u], z, acc, c4, a.alpha, a.gamma);
+        st4(a.W + (int64_t)(j + u * G) * a.ld + p0, w[u]);
+        if (matc) st4(a.C + (int64_t)(j + u * G) * a.ld + p0, c4);
+        bad |= !finite4(w[u]);
+      }
     }
     for (; j < a.r; j += G) {
       float4 w0 = ld_rw(a.W + (int64_t)j * a.ld + p0);
@@ -791,13 +793,24 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
     // 98k -> 102k with G = 2; C1 (d = 8k) and r = 32 are better with G = 4
     int G = (a.n4 * 2 >= 100000 && a.r <= 16) ? 2 : (a.r >= 4 ? 4 : 2);
     if (g_knob) G = g_knob;
+    // replicas per lane in flight: 4 when a lane has >= 4 of them (C2 k = 8:
+    // 161k -> 174k rounds/s, k = 16: 108k -> 118k; profiles/r01_split.jsonl),
+    // else 2; SMA_SPLIT_UJ = 2|4 forces it
+    static const int uj_knob = [] {
+      const char* e = getenv("SMA_SPLIT_UJ");
+      const int v = e ? atoi(e) : 0;
+      return (v == 2 || v == 4) ? v : 0;
+    }();
+    const int uj = uj_knob ? uj_knob : (a.r >= 4 * G ? 4 : 2);
     const int64_t cols_per_block = (kThreads / 32) * (32 / G);
     const int grid = (int)((a.n4 + cols_per_block - 1) / cols_per_block);
 #define SMA_SPLIT_LAUNCH(M)                                                                  \
   if (G == 16) e = launch_pdl(replica_step_split<M, 16>, grid, s, a);                         \
   else if (G == 8) e = launch_pdl(replica_step_split<M, 8>, grid, s, a);                      \
-  else if (G == 4) e = launch_pdl(replica_step_split<M, 4>, grid, s, a);                      \
-  else e = launch_pdl(replica_step_split<M, 2>, grid, s, a);
+  else if (G == 4) e = uj == 4 ? launch_pdl(replica_step_split<M, 4, 4>, grid, s, a)          \
+                               : launch_pdl(replica_step_split<M, 4>, grid, s, a);            \
+  else e = uj == 4 ? launch_pdl(replica_step_split<M, 2, 4>, grid, s, a)                      \
+                   : launch_pdl(replica_step_split<M, 2>, grid, s, a);
     cudaError_t e = cudaSuccess;
     switch (mode) {
       case kFused: SMA_SPLIT_LAUNCH(kFused) break;
