@@ -32,6 +32,38 @@ def build(force: bool = False) -> str:
     return _LIB
 
 
+_LIB_OMP = os.path.join(_HERE, "liboracle_sma_omp.so")
+_lib_omp = None
+
+
+def build_omp(force: bool = False) -> str:
+    """The same source with -fopenmp: adds orc_sma_run_synth_omp (bench timing only)."""
+    if force or not os.path.exists(_LIB_OMP) or os.path.getmtime(_LIB_OMP) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-ffp-contract=off", "-fPIC", "-fopenmp",
+                               "-shared", _SRC, "-o", _LIB_OMP, "-lm"])
+    return _LIB_OMP
+
+
+def run_synth_omp(d, k, alpha, gamma, mu, R, seed_w, seed_g, idx):
+    """run_synth (z, z_prev only) with the index set split over OpenMP threads;
+    bitwise equal to run_synth (separable per index).  Returns (z, z_prev, threads)."""
+    global _lib_omp
+    if _lib_omp is None:
+        build_omp()
+        L = C.CDLL(_LIB_OMP)
+        i32, i64, u64, f64, P = C.c_int32, C.c_int64, C.c_uint64, C.c_double, C.c_void_p
+        L.orc_sma_run_synth_omp.argtypes = [i64, i32, f64, f64, f64, i64, u64, u64, i64, P, P, P]
+        L.orc_sma_run_synth_omp.restype = C.c_int
+        _lib_omp = L
+    idx = _i64(idx)
+    z, zp = np.empty(idx.size), np.empty(idx.size)
+    nt = _lib_omp.orc_sma_run_synth_omp(d, k, alpha, gamma, mu, R, seed_w, seed_g, idx.size,
+                                        _p(idx), _p(z), _p(zp))
+    if nt < 0:
+        raise MemoryError("oracle allocation failed")
+    return z, zp, nt
+
+
 def lib():
     global _lib
     if _lib is None:

@@ -488,3 +488,29 @@ int orc_hier_run_synth(int64_t d, int32_t n, int32_t k, double alpha_l, double a
     free(W); free(U); free(G); free(part);
     return 0;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Host-parallel timing variant (SURVEY.md §8d "Oracle timing (ii)").        */
+/* Compiled only into liboracle_sma_omp.so (gcc -fopenmp): the sampled index */
+/* set is cut into contiguous chunks and each chunk runs orc_sma_run_synth   */
+/* unchanged on its own thread -- SMA with given gradients is separable per  */
+/* parameter index, so the result equals the single-thread run bit for bit.  */
+/* Returns the number of threads used, or -1 on allocation failure.          */
+/* ------------------------------------------------------------------------ */
+#ifdef _OPENMP
+#include <omp.h>
+int orc_sma_run_synth_omp(int64_t d, int32_t k, double alpha, double gamma, double mu,
+                          int64_t R, uint64_t seed_w, uint64_t seed_g,
+                          int64_t n_idx, const int64_t *idx, double *z_out, double *zprev_out) {
+    int nt = omp_get_max_threads();
+    int bad = 0;
+    #pragma omp parallel for schedule(static) reduction(|:bad)
+    for (int t = 0; t < nt; t++) {
+        int64_t lo = n_idx * t / nt, hi = n_idx * (t + 1) / nt;
+        if (hi > lo)
+            bad |= orc_sma_run_synth(d, k, alpha, gamma, mu, R, seed_w, seed_g, hi - lo, idx + lo,
+                                     z_out + lo, zprev_out + lo, NULL) != 0;
+    }
+    return bad ? -1 : nt;
+}
+#endif

@@ -497,3 +497,14 @@ def test_mlp_gradient_is_batch_mean(orc):
     _, g, _ = orc.mlp_loss_grad(X, y, rows, w)
     per = [orc.mlp_loss_grad(X, y, [r], w)[1] for r in rows]
     np.testing.assert_allclose(g, np.mean(per, axis=0), rtol=0, atol=1e-15)
+
+
+def test_openmp_timing_variant_equals_serial_oracle(orc):
+    """The host-parallel timing variant (bench cpu_baseline.all_cores) splits the
+    index set over threads; separability makes it bitwise equal to the serial
+    oracle."""
+    idx = np.arange(3, 50_000, 11)
+    z, zp, _ = orc.run_synth(50_000, 4, F32(0.25), F32(0.1), F32(0.9), 6, 1901, 2244, idx,
+                             want_W=False)
+    z2, zp2, nt = orc.run_synth_omp(50_000, 4, F32(0.25), F32(0.1), F32(0.9), 6, 1901, 2244, idx)
+    assert nt >= 1 and np.array_equal(z, z2) and np.array_equal(zp, zp2)
