@@ -358,7 +358,14 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
     a.nonfinite = h->check ? h->nonfinite : nullptr;
     STATUS_TRY(timer_pair(h, SMA_PHASE_FUSED_ZSYNC, &tp));
     if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
-    CUDA_TRY(launch_zsync_p2p(mode, a, 4 * h->num_sms, s));  // Mode B: high-priority stream
+    // persistent grid: SMA_P2P_CTAS_PER_SM x #SMs CTAs (default 4); in Mode B
+    // they share the SMs with the concurrent replica kernel
+    static const int per_sm = [] {
+      const char* e = getenv("SMA_P2P_CTAS_PER_SM");
+      const int v = e ? atoi(e) : 4;
+      return v >= 1 && v <= 8 ? v : 4;
+    }();
+    CUDA_TRY(launch_zsync_p2p(mode, a, per_sm * h->num_sms, s));  // Mode B: high-priority stream
     if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
     return SMA_OK;
   }
