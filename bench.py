@@ -64,6 +64,9 @@ def parse():
     ap.add_argument("--tau", type=int, default=1,
                     help="synchronise every tau iterations (sma_step_local on the others; "
                          "0 = never: the paper's 'no synchronisation' point, fig:overhead)")
+    ap.add_argument("--push", action="store_true",
+                    help="with the P2P z-sync: the replica kernel pushes each partial chunk into "
+                         "its owner's slot over peer memory (SMA_FLAG_P2P_PUSH)")
     ap.add_argument("--hier", action="store_true",
                     help="Section 3.3 two-level rule (per-GPU reference models, R20): "
                          "alpha_l = 1/(2r), alpha_g = 1/(2(N-1)); identical to flat SMA at N = 1")
@@ -289,6 +292,8 @@ def main():
         flags |= sma.FLAG_NVLS_ZSYNC
     if args.zsync in ("p2p", "auto") and collective:
         flags |= sma.FLAG_P2P_ZSYNC
+    if args.push and (flags & sma.FLAG_P2P_ZSYNC):
+        flags |= sma.FLAG_P2P_PUSH
     if args.hier:   # alpha is the intra-GPU alpha_l = 1/(2r); alpha_g keeps libsma's default
         flags |= sma.FLAG_HIERARCHICAL
         alpha = float(np.float32(1 / (2 * max(1, k // world))))
@@ -522,7 +527,8 @@ def main():
                        "mode": mode, "kernel": kvar,
                        "materialize_c": bool(args.matc), "hierarchical": bool(args.hier),
                        "parallelism": f"sma-dp{world}" + ("" if not collective else
-                                                           f"+{zsync}-zsync"),
+                                                           f"+{zsync}-zsync") +
+                                      ("-push" if flags & sma.FLAG_P2P_PUSH else ""),
                        "l2": "no flush: per-round working set "
                              f"{(alg_bytes / 1e9):.2f} GB/GPU >> 126 MB L2"},
             "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,

@@ -124,7 +124,15 @@ enum {
      * exactly the flat Alg. 1.  Every z-sync variant (NCCL, P2P, NVLS, Mode A/B)
      * carries it unchanged: only the per-GPU partial differs.  Not combined
      * with SMA_FLAG_MATERIALIZE_C or SMA_FLAG_KERNEL_TMA. */
-    SMA_FLAG_HIERARCHICAL = 1024u
+    SMA_FLAG_HIERARCHICAL = 1024u,
+    /* With SMA_FLAG_P2P_ZSYNC: fuse the reduce-scatter's data movement into the
+     * replica kernel.  Its epilogue stores each float4 chunk of the per-GPU
+     * partial straight into the owner's slot over peer memory (owner g's
+     * partial buffer holds one [shard] slot per source rank), so the z-sync
+     * kernel sums local slots in rank order instead of loading every peer's
+     * partial.  Same results bit for bit as SMA_FLAG_P2P_ZSYNC alone.  Not
+     * combined with SMA_FLAG_MATERIALIZE_C or SMA_FLAG_KERNEL_TMA. */
+    SMA_FLAG_P2P_PUSH = 2048u
 };
 
 typedef struct {

@@ -18,6 +18,12 @@ struct GradTable {
   const float* p[SMA_MAX_LOCAL_REPLICAS];
 };
 
+// SMA_FLAG_P2P_PUSH: where each rank's slot buffer of the current partial is
+// mapped in this process (owner g's buffer holds [n][shard] slots, one per source).
+struct PushTable {
+  float* p[SMA_MAX_LOCAL_REPLICAS];
+};
+
 // What the replica kernel emits besides the updated replicas.
 enum ReplicaMode : int {
   kFused = 0,    // n == 1: also z_next = z + sum c + mu (z - z_prev)   (Alg. 1 line 13)
@@ -50,6 +56,12 @@ struct ReplicaArgs {
   int64_t c0;          // first float4 chunk this launch covers (LDG tail after TMA)
   float* U;            // kHierA/B: this GPU's reference model u_g, updated in place [d_pad]
   float alpha_g;       // kHierA/B: inter-GPU correction weight
+  // SMA_FLAG_P2P_PUSH (push_n > 0): the per-GPU partial is not written to `out`
+  // but pushed, shard by shard, into slot `push_rank` of every owner's buffer
+  // (the reduce-scatter's data movement inside the replica kernel's epilogue)
+  PushTable push;
+  int64_t push_shard;  // floats per shard
+  int push_n, push_rank;
 };
 
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize, bytes) only when the size
@@ -74,6 +86,8 @@ cudaError_t launch_reduce_corrections(int mode, const ReplicaArgs& a, int num_sm
 cudaError_t launch_zsync(int mode, const float* S, const float* z, float* zprev_next,
                          int64_t n4, float alpha, float mu, float coef_b, int* nonfinite,
                          int num_sms, cudaStream_t s);
+// SMA_FLAG_P2P_PUSH: push a full local partial src [d_pad] into the owners' slots.
+cudaError_t launch_push_partial(const float* src, const ReplicaArgs& a, int num_sms, cudaStream_t s);
 // Mode B prologue: Q = scale * sum_j (w_j - zprev) over local replicas, or
 // Q = scale * (U - zprev) when U != nullptr (hierarchical, GPU g >= 1).
 cudaError_t launch_q_prologue(const float* W, int64_t ld, int r, const float* zprev, float* Q,
@@ -157,6 +171,7 @@ struct P2PArgs {
   int n, rank;
   unsigned* ctl;         // local: [0] barrier-A target, [1] barrier-B target, [2] CTA counter
   int* nonfinite;
+  int push;              // SMA_FLAG_P2P_PUSH: the partials are already in local slots
 };
 cudaError_t launch_zsync_p2p(int mode, const P2PArgs& a, int num_ctas, cudaStream_t s);
 

@@ -156,6 +156,18 @@ __device__ __forceinline__ float4 ld_ref(const ReplicaArgs& a, int64_t p0) {
   return ld_ro(a.z + p0);
 }
 
+// The per-GPU partial of a float4 column chunk: to `out`, or (SMA_FLAG_P2P_PUSH)
+// into slot push_rank of the owner of this chunk's shard -- a peer store over
+// NVLink for every shard but this GPU's own.
+__device__ __forceinline__ void store_partial(const ReplicaArgs& a, int64_t p0, float4 v) {
+  if (a.push_n > 0) {
+    const int g = (int)(p0 / a.push_shard);
+    st4(a.push.p[g] + (int64_t)a.push_rank * a.push_shard + (p0 - (int64_t)g * a.push_shard), v);
+  } else {
+    st4(a.out + p0, v);
+  }
+}
+
 // Section 3.3 / R20 on one component: c = alpha_g (u - z); u' = (u + D) - c.
 __device__ __forceinline__ float hier_ref_elem(float u, float D, float zc, float ag, float& c) {
   c = __fmul_rn(ag, __fsub_rn(u, zc));
@@ -180,13 +192,13 @@ __device__ __forceinline__ void replica_finish(const ReplicaArgs& a, int64_t p0,
       c.z = __fmul_rn(a.alpha_g, __fsub_rn(un.z, zc.z));
       c.w = __fmul_rn(a.alpha_g, __fsub_rn(un.w, zc.w));
     }
-    st4(a.out + p0, c);
+    store_partial(a, p0, c);
     bad |= !finite4(un);
     return;
   }
   if (MODE == kHierB0) {
-    st4(a.out + p0, make_float4(__fmul_rn(a.alpha, acc.x), __fmul_rn(a.alpha, acc.y),
-                                __fmul_rn(a.alpha, acc.z), __fmul_rn(a.alpha, acc.w)));
+    store_partial(a, p0, make_float4(__fmul_rn(a.alpha, acc.x), __fmul_rn(a.alpha, acc.y),
+                                     __fmul_rn(a.alpha, acc.z), __fmul_rn(a.alpha, acc.w)));
     return;
   }
   if (MODE == kFused) {
@@ -199,7 +211,7 @@ __device__ __forceinline__ void replica_finish(const ReplicaArgs& a, int64_t p0,
     st4(a.zprev_next + p0, zn);
     bad |= !finite4(zn);
   } else {
-    st4(a.out + p0, acc);
+    store_partial(a, p0, acc);
   }
 }
 
@@ -871,6 +883,19 @@ cudaError_t launch_zsync(int mode, const float* S, const float* z, float* zprev_
     k<<<grid_for(k, kThreads, 0, n4, num_sms), kThreads, 0, s>>>(S, z, zprev_next, n4, alpha, mu,
                                                                  coef_b, nonfinite);
   }
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(kThreads) push_partial_kernel(const float* __restrict__ src,
+                                                                const ReplicaArgs a) {
+  for (int64_t c = (int64_t)blockIdx.x * kThreads + threadIdx.x; c < a.n4;
+       c += (int64_t)gridDim.x * kThreads)
+    store_partial(a, c << 2, ld_ro(src + (c << 2)));
+}
+
+cudaError_t launch_push_partial(const float* src, const ReplicaArgs& a, int num_sms, cudaStream_t s) {
+  push_partial_kernel<<<grid_for(push_partial_kernel, kThreads, 0, a.n4, num_sms), kThreads, 0, s>>>(
+      src, a);
   return cudaGetLastError();
 }
 

@@ -105,14 +105,22 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
   const int64_t stride = (int64_t)gridDim.x * kP2PThreads;
   const float* zl = reinterpret_cast<const float*>(a.base[a.rank] + a.off_z);
   const float* zpl = reinterpret_cast<const float*>(a.base[a.rank] + a.off_zprev);
+  // source g's contribution to element e of this rank's shard: a peer load of
+  // g's partial, or (SMA_FLAG_P2P_PUSH: g's replica kernel already stored it into
+  // slot g of this rank's buffer) a local load
+  const float* mine = reinterpret_cast<const float*>(a.base[a.rank] + a.off_part);
+  const int64_t shard = a.len4 << 2, soff = a.off4 << 2;
+  auto part_ptr = [&](int g, int64_t e) -> const float* {
+    return a.push ? mine + (int64_t)g * shard + (e - soff)
+                  : reinterpret_cast<const float*>(a.base[g] + a.off_part) + e;
+  };
   // two chunks per iteration: 2n peer loads + 4 local loads in flight
   int64_t c = (int64_t)blockIdx.x * kP2PThreads + threadIdx.x;
   for (; c + stride < a.len4; c += 2 * stride) {
     const int64_t e0 = (a.off4 + c) << 2, e1 = (a.off4 + c + stride) << 2;
     float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
     for (int g = 0; g < n; ++g) {  // a6: the shard's sum over ranks, ascending rank
-      const float* pg = reinterpret_cast<const float*>(a.base[g] + a.off_part);
-      const float4 v0 = ld_ro4(pg + e0), v1 = ld_ro4(pg + e1);
+      const float4 v0 = ld_ro4(part_ptr(g, e0)), v1 = ld_ro4(part_ptr(g, e1));
       s0.x = __fadd_rn(s0.x, v0.x); s0.y = __fadd_rn(s0.y, v0.y);
       s0.z = __fadd_rn(s0.z, v0.z); s0.w = __fadd_rn(s0.w, v0.w);
       s1.x = __fadd_rn(s1.x, v1.x); s1.y = __fadd_rn(s1.y, v1.y);
@@ -132,7 +140,7 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
     const int64_t e = (a.off4 + c) << 2;  // element offset in the padded vector
     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int g = 0; g < n; ++g) {
-      const float4 v = ld_ro4(reinterpret_cast<const float*>(a.base[g] + a.off_part) + e);
+      const float4 v = ld_ro4(part_ptr(g, e));
       sum.x = __fadd_rn(sum.x, v.x); sum.y = __fadd_rn(sum.y, v.y);
       sum.z = __fadd_rn(sum.z, v.z); sum.w = __fadd_rn(sum.w, v.w);
     }

@@ -104,6 +104,8 @@ struct sma_handle {
   unsigned* nv_ctl = nullptr;  // [0..1] expect, [2] done counter (local memory)
   // P2P z-sync (CUDA IPC)
   bool p2p = false, p2p_connected = false;
+  bool push = false;            // SMA_FLAG_P2P_PUSH
+  float* push_scratch = nullptr;  // [d_pad] Mode B prologue staging (push mode)
   char* p2p_region = nullptr;
   size_t p2p_off_part = 0, p2p_off_z = 0;
   std::vector<char*> p2p_base;  // per rank, as mapped in this process
@@ -216,6 +218,7 @@ void free_all(sma_handle* h) {
   cudaFree(h->C);
   cudaFree(h->G);
   cudaFree(h->U);
+  cudaFree(h->push_scratch);
   cudaFree(h->nonfinite);
   for (int i = 0; i < 2; ++i) cudaFree(h->perm_dev[i]);
   cudaFree(h->mlp_A1);
@@ -279,6 +282,16 @@ sma_status timer_pair(sma_handle* h, int phase, cudaEvent_t** out) {
   return SMA_OK;
 }
 
+// SMA_FLAG_P2P_PUSH: the partial destined for local buffer `out` goes, shard by
+// shard, into slot `rank` of the same buffer on every rank (same region offsets).
+void fill_push(const sma_handle* h, const float* out, ReplicaArgs* a) {
+  const size_t off = (size_t)(reinterpret_cast<const char*>(out) - h->p2p_region);
+  for (int g = 0; g < h->cfg.world; ++g) a->push.p[g] = reinterpret_cast<float*>(h->p2p_base[g] + off);
+  a->push_n = h->cfg.world;
+  a->push_rank = h->cfg.rank;
+  a->push_shard = h->shard_len;
+}
+
 sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s, int sms = 0) {
   NvtxRange nvtx("sma.replica_kernel");
   if (sms <= 0) sms = h->num_sms;
@@ -299,6 +312,7 @@ sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s, i
   a.nonfinite = h->check ? h->nonfinite : nullptr;
   a.U = h->U;
   a.alpha_g = h->alpha_g;
+  if (h->push && out) fill_push(h, out, &a);
   cudaEvent_t* tp = nullptr;
   STATUS_TRY(timer_pair(h, SMA_PHASE_REPLICA, &tp));
   if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
@@ -312,6 +326,13 @@ sma_status replica_launch(sma_handle* h, int mode, float* out, cudaStream_t s, i
     }
   } else if (mode == kFused) {
     CUDA_TRY(launch_replica_step(mode, false, a, sms, s));  // z <- z + mu (z - z_prev)
+    ++h->launches;
+  } else if (h->push) {  // no local learners: push a zero partial
+    CUDA_TRY(cudaMemsetAsync(h->push_scratch, 0, sizeof(float) * h->d_pad, s));
+    ReplicaArgs z{};
+    z.n4 = h->n4;
+    fill_push(h, out, &z);
+    CUDA_TRY(launch_push_partial(h->push_scratch, z, h->num_sms, s));
     ++h->launches;
   } else {
     CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * h->d_pad, s));
@@ -356,6 +377,7 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
     a.rank = h->cfg.rank;
     a.ctl = h->p2p_ctl;
     a.nonfinite = h->check ? h->nonfinite : nullptr;
+    a.push = h->push ? 1 : 0;
     STATUS_TRY(timer_pair(h, SMA_PHASE_FUSED_ZSYNC, &tp));
     if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
     // persistent grid: SMA_P2P_CTAS_PER_SM x #SMs CTAs (default 4); in Mode B
@@ -408,6 +430,26 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
   if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
   NCCL_TRY(g_nccl.AllGather(h->zprev() + h->shard_off, h->zprev(), cnt, ncclFloat32, h->comm, s));
   if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
+  return SMA_OK;
+}
+
+// Mode B prologue: Q^i of the current state into Q[qi] --
+// or, with SMA_FLAG_P2P_PUSH, into the scratch buffer and from there into
+// slot `rank` of every owner's Q[qi].
+sma_status enqueue_q_prologue(sma_handle* h, cudaStream_t s) {
+  const float scale = !h->hier ? 1.f : (h->U ? h->alpha_g : h->alpha);
+  float* q = h->Q + (int64_t)h->qi * h->d_pad;
+  CUDA_TRY(launch_q_prologue(h->W, h->d_pad, h->r, h->zprev(), h->push ? h->push_scratch : q, h->n4,
+                             h->U, scale, h->num_sms, s));
+  ++h->launches;
+  if (h->push) {
+    ReplicaArgs a{};
+    a.n4 = h->n4;
+    fill_push(h, q, &a);
+    CUDA_TRY(launch_push_partial(h->push_scratch, a, h->num_sms, s));
+    ++h->launches;
+  }
+  h->q_dirty = false;
   return SMA_OK;
 }
 
@@ -497,6 +539,10 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
     return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_P2P_ZSYNC and SMA_FLAG_NVLS_ZSYNC are exclusive");
   if (h->p2p && !h->collective)
     return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_P2P_ZSYNC needs world > 1 or SMA_FLAG_FORCE_COLLECTIVE");
+  h->push = (f & SMA_FLAG_P2P_PUSH) != 0;
+  if (h->push && (!h->p2p || h->matc || (f & SMA_FLAG_KERNEL_TMA)))
+    return fail(SMA_ERR_INVALID_ARG,
+                "SMA_FLAG_P2P_PUSH needs SMA_FLAG_P2P_ZSYNC and excludes MATERIALIZE_C / KERNEL_TMA");
   if (h->p2p && cfg->world > kMaxP2PRanks)
     return fail(SMA_ERR_INVALID_ARG, "SMA_FLAG_P2P_ZSYNC supports at most %d ranks", kMaxP2PRanks);
   if (h->nvls && !h->collective)
@@ -574,6 +620,7 @@ sma_status create_impl(const sma_config* cfg, const float* w0, sma_handle* h) {
     CUDA_TRY(cudaMemset(h->p2p_ctl, 0, 4 * sizeof(unsigned)));
     h->p2p_base.assign(cfg->world, nullptr);
     h->p2p_base[cfg->rank] = h->p2p_region;
+    if (h->push) STATUS_TRY(alloc_zero(&h->push_scratch, dp));
     h->p2p_connected = cfg->world == 1;  // a single rank maps only itself
   } else if (h->nvls) {
     // [flags (4 KB) | P, or Q[2] | z[2]] bound to one multicast object per rank
@@ -734,13 +781,7 @@ sma_status sma_step(sma_handle* h, void* stream) {
       return fail(SMA_ERR_GRADS_MISSING, "learner %d has no registered gradient", h->j0 + i);
   DeviceGuard guard(h->dev);
   cudaStream_t s = (cudaStream_t)stream;
-  if (h->overlap && h->q_dirty) {
-    const float scale = !h->hier ? 1.f : (h->U ? h->alpha_g : h->alpha);
-    CUDA_TRY(launch_q_prologue(h->W, h->d_pad, h->r, h->zprev(), h->Q + (int64_t)h->qi * h->d_pad,
-                               h->n4, h->U, scale, h->num_sms, s));
-    ++h->launches;
-    h->q_dirty = false;
-  }
+  if (h->overlap && h->q_dirty) STATUS_TRY(enqueue_q_prologue(h, s));
   if (h->graphs && !h->timing && s != nullptr) {
     const int key = h->cur;
     if (!h->gexec[key] || h->gver[key] != h->ver) {
@@ -1153,14 +1194,7 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
       return fail(SMA_ERR_STATE, "SMA_FLAG_P2P_ZSYNC: call sma_p2p_connect on every rank first");
     DeviceGuard guard(h->dev);
     cudaStream_t s = (cudaStream_t)stream;
-    if (h->q_dirty) {
-      const float scale = !h->hier ? 1.f : (h->U ? h->alpha_g : h->alpha);
-      CUDA_TRY(launch_q_prologue(h->W, h->d_pad, h->r, h->zprev(),
-                                 h->Q + (int64_t)h->qi * h->d_pad, h->n4, h->U, scale,
-                                 h->num_sms, s));
-      ++h->launches;
-      h->q_dirty = false;
-    }
+    if (h->q_dirty) STATUS_TRY(enqueue_q_prologue(h, s));
     const LearnerFn fn = [&](cudaStream_t ls) { return sma_learner_grads(h, round, ls); };
     STATUS_TRY(enqueue_round(h, s, &fn));
     advance(h);

@@ -27,6 +27,7 @@ FLAG_KERNEL_LDG = 128
 FLAG_NVLS_ZSYNC = 256
 FLAG_P2P_ZSYNC = 512
 FLAG_HIERARCHICAL = 1024
+FLAG_P2P_PUSH = 2048
 P2P_HANDLE_BYTES = 64
 MAX_LOCAL_REPLICAS = 64
 NCCL_ID_BYTES = 128

@@ -57,6 +57,9 @@ COLLECTIVE_FLAGS = {
     "p2pA_matc": 16 | 2 | 512,
     "p2pB": 16 | 1 | 512,
     "p2pB_graph": 16 | 1 | 8 | 512,
+    "pushA": 16 | 512 | 2048,
+    "pushB": 16 | 1 | 512 | 2048,
+    "pushB_graph": 16 | 1 | 8 | 512 | 2048,
 }
 
 

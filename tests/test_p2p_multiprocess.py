@@ -276,3 +276,55 @@ def test_p2p_hierarchical_checkpoint_tau_restart(orc, tmp_path, mode):
         assert rel(np.load(tmp_path / f"u{r}.npy"), st.U[r]) <= 1e-5
     for j in range(k):
         assert rel(np.load(tmp_path / f"w{j}.npy"), st.W[j]) <= 1e-5
+
+
+@pytest.mark.parametrize("world,k", [(2, 4), (3, 7), (4, 8)])
+@pytest.mark.parametrize("mode", ["A", "B", "B_graph"])
+def test_p2p_push_equals_pull_bitwise(orc, tmp_path, world, k, mode):
+    """SMA_FLAG_P2P_PUSH (the replica kernel's epilogue stores each partial chunk
+    into its owner's slot over peer memory; the z-sync sums local slots) gives
+    the same bits as the pull z-sync (peer loads of every partial), and both
+    match the oracle; 2-4 ranks as processes on one GPU, uneven splits."""
+    import torch.multiprocessing as mp
+
+    import sma_inputs
+    from paper_1901_02244_b200 import sma
+    flags = {"A": 0, "B": 1, "B_graph": 1 | 8}[mode]
+    d, R = 100_003, 12
+    res = {}
+    for push in (0, sma.FLAG_P2P_PUSH):
+        out = tmp_path / f"p{push}"
+        out.mkdir()
+        mp.spawn(_worker, args=(world, _port(), flags | push, d, k, R, str(out)), nprocs=world)
+        res[push] = out
+    for g in range(world):
+        assert np.array_equal(np.load(res[0] / f"z{g}.npy"), np.load(res[sma.FLAG_P2P_PUSH] / f"z{g}.npy"))
+    for j in range(k):
+        assert np.array_equal(np.load(res[0] / f"w{j}.npy"), np.load(res[sma.FLAG_P2P_PUSH] / f"w{j}.npy"))
+    zr, _, _ = orc.run_synth(d, k, float(np.float32(1 / k)), float(np.float32(0.1)),
+                             float(np.float32(0.9)), R, sma_inputs.SEED_W, sma_inputs.SEED_G,
+                             want_W=False)
+    z = np.load(res[sma.FLAG_P2P_PUSH] / "z0.npy")
+    assert np.max(np.abs(z - zr) / (1 + np.abs(zr))) <= 1e-5
+
+
+@pytest.mark.parametrize("mode", ["A", "B"])
+def test_p2p_push_hierarchical_matches_oracle(orc, tmp_path, mode):
+    """The push epilogue also carries the two-level rule's partials (kHierA/B/B0)."""
+    import torch.multiprocessing as mp
+
+    import sma_inputs
+    from paper_1901_02244_b200 import sma
+    world, k, d, R = 3, 7, 100_003, 12
+    al = float(np.float32(0.25))
+    mp.spawn(_hier_worker, args=(world, _port(), {"A": 0, "B": 1}[mode] | sma.FLAG_P2P_PUSH, d, k, R,
+                                 al, None, False, str(tmp_path)), nprocs=world)
+    f = lambda x: float(np.float32(x))  # noqa: E731
+    zr, _, Wr, Ur = orc.hier_run_synth(d, world, k, al, f(1 / (2 * (world - 1))), f(0.1), f(0.9), R,
+                                       sma_inputs.SEED_W, sma_inputs.SEED_G)
+    rel = lambda x, y: np.max(np.abs(x - y) / (1 + np.abs(y)))  # noqa: E731
+    assert rel(np.load(tmp_path / "z0.npy"), zr) <= 1e-5
+    for g in range(1, world):
+        assert rel(np.load(tmp_path / f"u{g}.npy"), Ur[g]) <= 1e-5
+    for j in range(k):
+        assert rel(np.load(tmp_path / f"w{j}.npy"), Wr[j]) <= 1e-5
