@@ -47,6 +47,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [nvcc, *ARCH, "-lineinfo", "-O3", "-std=c++17", "-Xcompiler", "-fPIC",
            "-shared", "-cudart", "static", f"-I{_nccl_include()}", f"-I{os.path.join(ROOT, 'include')}",
            *sources(), "-o", LIB + ".tmp", "-ldl"]
+    extra = os.environ.get("SMA_NVCC_EXTRA")   # experiments only, e.g. -DSMA_SPLIT_MINB=1
+    if extra:
+        cmd[1:1] = extra.split()
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd))

@@ -281,8 +281,12 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) replica_step_ldg(const R
 // j = g, g + G, ... (two per load batch), and the G partial sums are combined
 // with log2(G) xor-shuffles (bitwise identical in every lane: fp addition is
 // commutative); group 0 finishes the column.  4x the threads for the same d.
+#ifndef SMA_SPLIT_MINB
+#define SMA_SPLIT_MINB 4
+#endif
+constexpr int kSplitMinBlocks = SMA_SPLIT_MINB;  // resident CTAs per SM the register budget allows
 template <int MODE, int G, int UJ = 2>
-__global__ void __launch_bounds__(kThreads) replica_step_split(const ReplicaArgs a) {
+__global__ void __launch_bounds__(kThreads, kSplitMinBlocks) replica_step_split(const ReplicaArgs a) {
   pdl::wait_and_release();
   constexpr int CPW = 32 / G;  // columns per warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
