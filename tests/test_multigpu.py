@@ -65,7 +65,8 @@ def _worker(rank, world, port, flags, d, k, R, out):
 
 
 @pytest.mark.skipif(_ngpus() < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("flags", [0, 1, 8, 1 | 8, 256, 1 | 256, 512, 1 | 512, 1 | 8 | 512])
+@pytest.mark.parametrize("flags", [0, 1, 8, 1 | 8, 256, 1 | 256, 512, 1 | 512, 1 | 8 | 512, 512 | 2048,
+                                   1 | 512 | 2048])
 def test_multi_gpu_matches_oracle(orc, tmp_path, flags):
     import torch.multiprocessing as mp
 
