@@ -299,7 +299,7 @@ sma_status sma_check_finite(sma_handle* h, int* flag);
  * classes*in_dim + classes; kind 1 = MLP in_dim-hidden-classes with ReLU
  * (NEXT-2), params W1 [hidden][in_dim], b1 [hidden], W2 [classes]
  * [hidden], b2 [classes], d = hidden*in_dim + hidden + classes*hidden + classes
- * (the ReLU mask is decided on fp64 pre-activations, R18).  X_dev: n_samples x in_dim fp32
+ * (the ReLU mask is decided at fp64-level accuracy, R18).  X_dev: n_samples x in_dim fp32
  * row-major, y_dev: n_samples int32 labels in [0, classes); both on this
  * rank's device and BORROWED for the handle's lifetime.  batch = b rows per
  * learner per round; batch_seed keys the per-epoch permutation (R10).
@@ -310,8 +310,10 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
 
 /* For every local learner j: gather batch B(round, j) (R10), compute the
  * batch-mean gradient (Eq. 2) of the mean cross-entropy at the
- * current replica w_j (max-subtracted softmax, R16) in fp32 FFMA (no TF32;
- * MLP first-layer pre-activations in fp64),
+ * current replica w_j (max-subtracted softmax, R16) in fp32 (FFMA; for the MLP
+ * with >= 10 local learners its two 784x256 GEMMs run on the tensor cores as
+ * 3xTF32, SMA_MLP_TC; the ReLU mask is certain at fp64-level accuracy either
+ * way: an a-priori error bound, and a double-float recomputation near a kink),
  * into the handle's gradient buffer, and register it.  Enqueued on
  * cuda_stream.  Errors: STATE (no learner attached), CUDA. */
 sma_status sma_learner_grads(sma_handle* h, int64_t round, void* cuda_stream);
