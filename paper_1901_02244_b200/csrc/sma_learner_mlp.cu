@@ -260,11 +260,42 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_w1_kernel(
   }
   __syncthreads();
   const float fb = (float)b;
-  for (int q = threadIdx.x; q < nu * nf; q += blockDim.x) {  // dW1 = da^T x / b
-    const int u = q / nf, f = q - u * nf;
-    float s = 0.f;
-    for (int t = 0; t < b; ++t) s = __fmaf_rn(da[t * nu + u], xs[t * nf + f], s);
-    G[(int64_t)(k0 + u) * in_dim + f0 + f] = __fdiv_rn(s, fb);
+  // / b as * 2^-log2(b) when b is a power of two: both are the correctly
+  // rounded s / b, so the result is bitwise the same and the IEEE division's
+  // instruction sequence (the kernel is issue-bound) is gone
+  const bool pow2 = (b & (b - 1)) == 0;
+  const float inv_b = 1.f / fb;
+  if ((in_dim & 3) == 0 && (ld & 3) == 0) {
+    // 4 adjacent features per thread: one da load and one 128-bit x load per
+    // 4 FMAs, one 128-bit store; per output the same ascending-t FMA chain
+    const int nf4 = nf >> 2;
+    for (int q = threadIdx.x; q < nu * nf4; q += blockDim.x) {  // dW1 = da^T x / b
+      const int u = q / nf4, f = (q - u * nf4) << 2;
+      float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int t = 0; t < b; ++t) {
+        const float a = da[t * nu + u];
+        const float4 x = *reinterpret_cast<const float4*>(xs + t * nf + f);
+        s.x = __fmaf_rn(a, x.x, s.x);
+        s.y = __fmaf_rn(a, x.y, s.y);
+        s.z = __fmaf_rn(a, x.z, s.z);
+        s.w = __fmaf_rn(a, x.w, s.w);
+      }
+      if (pow2) {
+        s.x = __fmul_rn(s.x, inv_b); s.y = __fmul_rn(s.y, inv_b);
+        s.z = __fmul_rn(s.z, inv_b); s.w = __fmul_rn(s.w, inv_b);
+      } else {
+        s.x = __fdiv_rn(s.x, fb); s.y = __fdiv_rn(s.y, fb);
+        s.z = __fdiv_rn(s.z, fb); s.w = __fdiv_rn(s.w, fb);
+      }
+      *reinterpret_cast<float4*>(G + (int64_t)(k0 + u) * in_dim + f0 + f) = s;
+    }
+  } else {
+    for (int q = threadIdx.x; q < nu * nf; q += blockDim.x) {  // dW1 = da^T x / b
+      const int u = q / nf, f = q - u * nf;
+      float s = 0.f;
+      for (int t = 0; t < b; ++t) s = __fmaf_rn(da[t * nu + u], xs[t * nf + f], s);
+      G[(int64_t)(k0 + u) * in_dim + f0 + f] = pow2 ? __fmul_rn(s, inv_b) : __fdiv_rn(s, fb);
+    }
   }
   if (blockIdx.z == 0 && threadIdx.x < nu) {
     float s = 0.f;
