@@ -495,18 +495,33 @@ using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t
 EncodeTiledFn g_encode = nullptr;
 std::once_flag g_encode_once;
 
-// SMA_MLP_TC: 0 = SIMT kernels, 1 = tensor cores, unset = by learners per GPU:
-// measured (profiles/r01_mlp_tc_sweep.txt, MLP rounds/s, b = 16, PDL on) the two
-// tensor-core GEMMs (layer 1 + dW1) lose while the SIMT kernels' many small CTAs
-// still fit the GPU (k = 4: 32.1k SIMT vs 25.8k; k = 8: 21.9k vs 20.5k; 56 CTAs of
-// short latency phases) and win from r = 10 on (19.8k vs 17.9k; r = 16: 16.0k
-// vs 13.4k).
+// SMA_MLP_TC: 0 = SIMT kernels, 1 = both GEMMs on the tensor cores, "hidden" =
+// layer 1 only, "w1" = dW1 only; unset = by learners per GPU (tc_wanted()).
+// Bits: 1 = layer 1, 2 = dW1; -1 = unset.
 int tc_policy() {
   static const int p = [] {
     const char* e = getenv("SMA_MLP_TC");
-    return e ? (e[0] == '0' ? 0 : 1) : -1;
+    if (!e) return -1;
+    if (e[0] == 'h') return 1;
+    if (e[0] == 'w') return 2;
+    return e[0] == '0' ? 0 : 3;
   }();
   return p;
+}
+
+// Default thresholds, measured (profiles/r01_mlp_tc_sweep2.txt, MLP rounds/s,
+// b = 16, PDL on, SIMT vs tensor cores per GEMM): layer 1 on tcgen05 loses while
+// the SIMT kernel's 64 CTAs per learner still fit one wave (k = 4: 38.7k SIMT vs
+// 34.4k; k = 8: 27.1k vs 24.2k) and wins from r = 12 on (20.9k vs 20.6k; k = 16:
+// 16.8k vs 16.5k; k = 32: 10.2k vs 9.8k). The SIMT dW1 kernel (4 features per
+// thread) is at least as fast as the tensor-core one at every k measured (4-32),
+// so dW1 takes the tensor cores only when forced (SMA_MLP_TC=1 / w1).
+constexpr int kTcHiddenMinR = 12;         // layer 1
+constexpr int kTcW1MinR = 1 << 30;        // dW1: never by default
+bool tc_wanted(int bit, int r) {
+  const int pol = tc_policy();
+  if (pol >= 0) return (pol & bit) != 0;
+  return r >= (bit == 1 ? kTcHiddenMinR : kTcW1MinR);
 }
 }  // namespace
 
@@ -516,8 +531,7 @@ int tc_policy() {
 cudaError_t launch_mlp_hidden_tc(const float* X, const int32_t* perm, int64_t pos0, int b,
                                  int in_dim, int hidden, const float* W, int64_t ld, int r, int j0,
                                  float2* A1, cudaStream_t s) {
-  const int pol = tc_policy();
-  if (pol == 0 || (pol < 0 && r < 10) || b > kTcN || b < 1 || hidden % kTcM != 0 || hidden > 65535 ||
+  if (!tc_wanted(1, r) || b > kTcN || b < 1 || hidden % kTcM != 0 || hidden > 65535 ||
       (in_dim & 3) != 0 || in_dim > kMaxCluster * kTcKC || r < 1)
     return cudaErrorNotSupported;
   std::call_once(g_encode_once, [] {
@@ -569,8 +583,7 @@ namespace sma {
 cudaError_t launch_mlp_w1_tc(const float* X, const int32_t* perm, int64_t pos0, int b, int in_dim,
                              int hidden, int j0, int64_t ld, int r, const float* DA, float* G,
                              cudaStream_t s) {
-  const int pol = tc_policy();
-  if (pol == 0 || (pol < 0 && r < 10) || b < 1 || b > kBoxK || hidden % kTcM != 0 ||
+  if (!tc_wanted(2, r) || b < 1 || b > kBoxK || hidden % kTcM != 0 ||
       (in_dim & 3) != 0 || r < 1)
     return cudaErrorNotSupported;
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_w1_tc_kernel), kW1Smem);

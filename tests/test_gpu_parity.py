@@ -700,7 +700,9 @@ def test_learner_step_overlapped_zsync(torch_cuda, S, orc, kind, variant):
 def test_mlp_layer1_tensor_cores_vs_simt_and_oracle(torch_cuda, orc, tmp_path, k, b):
     """NEXT-2: the MLP's layer-1 GEMM on tcgen05 (3xTF32 + |.|-bound MMAs, K split
     over a 7-CTA cluster; SMA_MLP_TC=1) and the SIMT kernel (SMA_MLP_TC=0) give
-    the same gradients to ~1e-7 and both match the fp64 oracle < 2e-6 (ragged
+    the same gradients to ~1e-7 -- so do the mixed policies (layer 1 only:
+    "hidden", the default from r >= 12; dW1 only: "w1") -- and all match the
+    fp64 oracle < 2e-6 (ragged
     batch b = 5 pads N = 16 with zero rows); the ReLU mask is decided at
     fp64-level accuracy on both paths (R18)."""
     import os
@@ -710,7 +712,8 @@ def test_mlp_layer1_tensor_cores_vs_simt_and_oracle(torch_cuda, orc, tmp_path, k
     X, y = sma_inputs.blobs(2_000, seed=12)
     rnd, seed = 7, 31
     got = {}
-    for tc in ("0", "1"):
+    modes = ("0", "1", "hidden", "w1")
+    for tc in modes:
         out = str(tmp_path / f"g{tc}.npy")
         env = dict(os.environ, SMA_MLP_TC=tc)
         subprocess.check_call([sys.executable, worker, out, str(k), str(b), str(rnd), str(seed)],
@@ -723,6 +726,7 @@ def test_mlp_layer1_tensor_cores_vs_simt_and_oracle(torch_cuda, orc, tmp_path, k
         rows = orc.batch_indices(X.shape[0], k, b, 21, rnd, j)
         _, gref, margin = orc.mlp_loss_grad(X, y, rows, w0)
         assert margin > 1e-9
-        for tc in ("0", "1"):
+        for tc in modes:
             assert np.max(np.abs(got[tc][j] - gref)) < 2e-6, (tc, j)
-    assert np.max(np.abs(got["0"] - got["1"])) < 1e-6
+    for tc in modes[1:]:
+        assert np.max(np.abs(got["0"] - got[tc])) < 1e-6, tc
