@@ -311,9 +311,10 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
 /* For every local learner j: gather batch B(round, j) (R10), compute the
  * batch-mean gradient (Eq. 2) of the mean cross-entropy at the
  * current replica w_j (max-subtracted softmax, R16) in fp32 (FFMA; for the MLP
- * with >= 12 local learners its layer-1 784x256 GEMM runs on the tensor cores
- * as 3xTF32, SMA_MLP_TC; the ReLU mask is certain at fp64-level accuracy either
- * way: an a-priori error bound, and a double-float recomputation near a kink),
+ * with >= 12 local learners, unless its SIMT grid fills a wave, its layer-1
+ * 784x256 GEMM runs on the tensor cores as 3xTF32, SMA_MLP_TC; the ReLU
+ * mask is certain at fp64-level accuracy either way: an a-priori error
+ * bound, and a double-float recomputation near a kink),
  * into the handle's gradient buffer, and register it.  Enqueued on
  * cuda_stream.  Errors: STATE (no learner attached), CUDA. */
 sma_status sma_learner_grads(sma_handle* h, int64_t round, void* cuda_stream);

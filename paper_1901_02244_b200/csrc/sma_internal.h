@@ -114,6 +114,8 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
                             int b, int in_dim, int hidden, int classes, const float* W, int64_t ld,
                             int r, int j0, float2* A1, float* E, float* DA, float* G,
                             cudaStream_t s);
+// SMA_MLP_TC as parsed: -1 unset (per-r defaults), else bits 1 = layer 1, 2 = dW1.
+int mlp_tc_policy();
 // MLP layer 1 on tcgen05 (3xTF32 + |.| bound MMAs, cluster K-split); returns
 // cudaErrorNotSupported without launching when the shape is outside its path.
 cudaError_t launch_mlp_hidden_tc(const float* X, const int32_t* perm, int64_t pos0, int b,

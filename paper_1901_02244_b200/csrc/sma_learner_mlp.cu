@@ -16,6 +16,7 @@
 // fp32 FFMA elsewhere; no TF32.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "sma_bulk.cuh"
 #include "sma_dot2.cuh"
@@ -26,7 +27,8 @@
 namespace sma {
 namespace {
 constexpr int kUnits = 16;       // hidden units per CTA of the dW1 kernel
-constexpr int kHidUnits = 4;     // hidden units per CTA of the forward kernel
+constexpr int kHidUnits = 4;     // hidden units per CTA of the forward kernel (fallback)
+constexpr int kMaxHidUnits = 16;
 constexpr int kRowBatch = 8;     // batch rows per warp of the forward kernel (independent chains)
 constexpr int kMlpThreads = 256;
 constexpr int kHeadSplit = 16;   // CTAs per learner of the head-gradient kernel
@@ -41,14 +43,15 @@ using dot2::f2_add;
 
 __global__ void __launch_bounds__(kMlpThreads, 1) mlp_hidden_kernel(
     const float* __restrict__ X, const int32_t* __restrict__ perm, int64_t pos0, int b, int in_dim,
-    int hidden, const float* __restrict__ Wall, int64_t ld, int j0, float2* __restrict__ A1) {
+    int hidden, const float* __restrict__ Wall, int64_t ld, int j0, float2* __restrict__ A1,
+    int hid_units) {
   // R18: the pre-activation that decides the ReLU mask is accumulated in
   // double-float (hi + lo), accurate to ~2^-48 like the oracle's fp64.
   extern __shared__ __align__(16) float sm[];
   float* xs = sm;                                // [b][in_dim]
-  float* ws = xs + (int64_t)b * in_dim;          // [kHidUnits][in_dim]
-  const int slot = blockIdx.x, k0 = blockIdx.y * kHidUnits;
-  const int nu = min(kHidUnits, hidden - k0);
+  float* ws = xs + (int64_t)b * in_dim;          // [hid_units][in_dim]
+  const int slot = blockIdx.x, k0 = blockIdx.y * hid_units;
+  const int nu = min(hid_units, hidden - k0);
   const float* W1 = Wall + (int64_t)slot * ld;
   const float* b1 = W1 + (int64_t)hidden * in_dim;
   __shared__ int rows[64];
@@ -310,7 +313,55 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
                             int r, int j0, float2* A1, float* E, float* DA, float* G,
                             cudaStream_t s) {
   if (classes > 32) return cudaErrorInvalidValue;
-  const size_t sm1 = sizeof(float) * ((size_t)b * in_dim + (size_t)kHidUnits * in_dim);
+  // Hidden units per CTA of the SIMT layer-1 kernel: the fewest (1, 2, 4, 8, 16)
+  // whose grid r x ceil(hidden / u) still fits one wave at the kernel's occupancy.
+  // Measured (profiles/r01_mlp_hid_units.txt, MLP rounds/s, SIMT): k = 4 best at
+  // u = 4 (256 CTAs; 39.0k vs 31.6k at 2, 32.8k at 8), k = 8 at u = 8 (256 CTAs;
+  // 28.8k vs 27.2k at 4): more CTAs than one wave re-stage the batch rows in a
+  // second wave, fewer leave the per-CTA chain longer. SMA_MLP_HID_UNITS forces u.
+  static const int env_units = [] {
+    const char* v = getenv("SMA_MLP_HID_UNITS");
+    const int u = v ? atoi(v) : 0;
+    return u >= 1 && u <= kMaxHidUnits ? u : 0;
+  }();
+  int hid_units = env_units;
+  bool simt_fills = false;
+  if (!hid_units) {
+    struct UnitsCache {
+      int dev = -1, r = 0, b = 0, in_dim = 0, hidden = 0, units = kHidUnits;
+      bool fills = false;  // the grid fills >= 85 % of one wave
+    };
+    thread_local UnitsCache uc;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (uc.dev != dev || uc.r != r || uc.b != b || uc.in_dim != in_dim || uc.hidden != hidden) {
+      int sms = 0;
+      if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess)
+        return e;
+      int units = kMaxHidUnits;
+      bool fills = false;
+      for (int u = 1; u <= kMaxHidUnits; u *= 2) {
+        const size_t smu = sizeof(float) * ((size_t)b * in_dim + (size_t)u * in_dim);
+        if (ensure_dyn_smem(reinterpret_cast<const void*>(mlp_hidden_kernel), (int)smu) != cudaSuccess)
+          break;
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, mlp_hidden_kernel, kMlpThreads, smu) !=
+            cudaSuccess)
+          break;
+        const int64_t ctas = (int64_t)r * ((hidden + u - 1) / u), slots = (int64_t)occ * sms;
+        if (ctas <= slots) {
+          units = u;
+          fills = ctas * 100 >= slots * 85;
+          break;
+        }
+      }
+      uc = UnitsCache{dev, r, b, in_dim, hidden, units, fills};
+    }
+    hid_units = uc.units;
+    simt_fills = uc.fills;
+  }
+  const size_t sm1 = sizeof(float) * ((size_t)b * in_dim + (size_t)hid_units * in_dim);
   const size_t smL = sizeof(float) * (size_t)hidden;
   const size_t sm2 = sizeof(float) * ((size_t)b * hidden + (size_t)classes * hidden +
                                       (size_t)b * classes) +
@@ -321,14 +372,18 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
     return e;
   if ((e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_head_kernel), (int)sm2)) != cudaSuccess)
     return e;
-  const dim3 g1(r, (hidden + kHidUnits - 1) / kHidUnits), gL(r, b), g2(r, kHeadSplit),
+  const dim3 g1(r, (hidden + hid_units - 1) / hid_units), gL(r, b), g2(r, kHeadSplit),
       g3(r, (hidden + kUnits - 1) / kUnits, (in_dim + kFeat - 1) / kFeat);
   // layer 1 on the tensor cores (sma_learner_mlp_tc.cu) where the shape allows,
   // else the SIMT kernel; both write the same A1 contract
-  e = launch_mlp_hidden_tc(X, perm, pos0, b, in_dim, hidden, W, ld, r, j0, A1, s);
+  // (default policy: a SIMT grid that fills one wave beats the tensor cores even
+  // at r >= 12 -- k = 16: 18.4k vs 16.8k rounds/s, profiles/r01_mlp_hid_units2.txt)
+  e = (mlp_tc_policy() < 0 && simt_fills)
+          ? cudaErrorNotSupported
+          : launch_mlp_hidden_tc(X, perm, pos0, b, in_dim, hidden, W, ld, r, j0, A1, s);
   if (e == cudaErrorNotSupported)
     e = pdl::launch(mlp_hidden_kernel, g1, dim3(kMlpThreads), sm1, s, 1, X, perm, pos0, b, in_dim,
-                    hidden, W, ld, j0, A1);
+                    hidden, W, ld, j0, A1, hid_units);
   if (e != cudaSuccess) return e;
   if ((e = pdl::launch(mlp_logits_kernel, gL, dim3(kMlpThreads), smL, s, 1, y, perm, pos0, b, in_dim,
                        hidden, classes, W, ld, j0, (const float2*)A1, E)) != cudaSuccess)

@@ -516,7 +516,8 @@ int tc_policy() {
 // 16.8k vs 16.5k; k = 32: 10.2k vs 9.8k). The SIMT dW1 kernel (4 features per
 // thread) is at least as fast as the tensor-core one at every k measured (4-32),
 // so dW1 takes the tensor cores only when forced (SMA_MLP_TC=1 / w1).
-constexpr int kTcHiddenMinR = 12;         // layer 1
+constexpr int kTcHiddenMinR = 12;         // layer 1 (launch_mlp_grad also keeps the SIMT
+                                          // kernel when its grid fills >= 85 % of a wave)
 constexpr int kTcW1MinR = 1 << 30;        // dW1: never by default
 bool tc_wanted(int bit, int r) {
   const int pol = tc_policy();
@@ -524,6 +525,8 @@ bool tc_wanted(int bit, int r) {
   return r >= (bit == 1 ? kTcHiddenMinR : kTcW1MinR);
 }
 }  // namespace
+
+int mlp_tc_policy() { return tc_policy(); }
 
 // Returns cudaErrorNotSupported (nothing launched) when the policy or the shape
 // keeps layer 1 on the SIMT kernel (tc_policy(); b > 16, hidden % 128, in_dim % 4,
