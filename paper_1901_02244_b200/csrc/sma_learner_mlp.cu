@@ -156,16 +156,20 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_logits_kernel(
     const int32_t* __restrict__ y, const int32_t* __restrict__ perm, int64_t pos0, int b,
     int in_dim, int hidden, int classes, const float* __restrict__ Wall, int64_t ld, int j0,
     const float2* __restrict__ A1, float* __restrict__ E) {
-  pdl::wait_and_release();
   extern __shared__ __align__(16) float sm[];
   float* hrow = sm;                 // [hidden]
+  float* w2s = sm + hidden;         // [classes][hidden] + b2 [classes]
   __shared__ float lg[32];
   const int slot = blockIdx.x, t = blockIdx.y;
   const float* W2 = Wall + (int64_t)slot * ld + (int64_t)hidden * in_dim + hidden;
-  const float* b2 = W2 + (int64_t)classes * hidden;
   const float2* a1 = A1 + ((int64_t)slot * b + t) * hidden;
   __shared__ int yt_sm;
   if (threadIdx.x == 0) yt_sm = y[batch_row(perm, pos0, j0 + slot, b, t)];  // early: off the tail
+  // W2 and b2 before the wait: the replicas were last written by the previous
+  // round's replica kernel, which the layer-1 kernel's own wait (before it
+  // released this grid) already saw complete; only A1 is the predecessor's output
+  for (int q = threadIdx.x; q < classes * hidden + classes; q += blockDim.x) w2s[q] = __ldg(W2 + q);
+  pdl::wait_and_release();
   for (int k = threadIdx.x; k < hidden; k += blockDim.x) {  // relu of the double-float a1
     const float2 v = a1[k];
     hrow[k] = (v.x > 0.f || (v.x == 0.f && v.y > 0.f)) ? __fadd_rn(v.x, v.y) : 0.f;
@@ -174,10 +178,10 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_logits_kernel(
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   for (int c = warp; c < classes; c += nw) {
     float s = 0.f;
-    for (int k = lane; k < hidden; k += 32) s = __fmaf_rn(__ldg(W2 + (int64_t)c * hidden + k), hrow[k], s);
+    for (int k = lane; k < hidden; k += 32) s = __fmaf_rn(w2s[c * hidden + k], hrow[k], s);
 #pragma unroll
     for (int off = 16; off >= 1; off >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
-    if (lane == 0) lg[c] = __fadd_rn(s, b2[c]);
+    if (lane == 0) lg[c] = __fadd_rn(s, w2s[classes * hidden + c]);
   }
   __syncthreads();
   if (threadIdx.x < 32)  // max-subtracted softmax, e = p - onehot(y_t)
@@ -362,13 +366,15 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
     simt_fills = uc.fills;
   }
   const size_t sm1 = sizeof(float) * ((size_t)b * in_dim + (size_t)hid_units * in_dim);
-  const size_t smL = sizeof(float) * (size_t)hidden;
+  const size_t smL = sizeof(float) * ((size_t)hidden + (size_t)classes * hidden + classes);
   const size_t sm2 = sizeof(float) * ((size_t)b * hidden + (size_t)classes * hidden +
                                       (size_t)b * classes) +
                      16 + sizeof(float2) * (size_t)b * hidden;
   const size_t sm3 = sizeof(float) * ((size_t)b * kFeat + (size_t)b * kUnits);
   cudaError_t e;
   if ((e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_hidden_kernel), (int)sm1)) != cudaSuccess)
+    return e;
+  if ((e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_logits_kernel), (int)smL)) != cudaSuccess)
     return e;
   if ((e = ensure_dyn_smem(reinterpret_cast<const void*>(mlp_head_kernel), (int)sm2)) != cudaSuccess)
     return e;
