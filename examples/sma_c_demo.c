@@ -2,11 +2,12 @@
  *
  * Build:  gcc -O2 -I include examples/sma_c_demo.c -L paper_1901_02244_b200 -lsma \
  *             -Wl,-rpath,$PWD/paper_1901_02244_b200 -o sma_c_demo
- * Run:    ./sma_c_demo [d] [k] [rounds]
+ * Run:    ./sma_c_demo [d] [k] [rounds] [z_out.bin]
  * Creates an SMA handle (Alg. 1, arXiv 1901.02244) with w0 = 0, registers the
  * handle's synthetic gradients each round, runs `rounds` rounds on the legacy
- * stream and prints z[0..3] and the replica-kernel time.  Exit code 0 on
- * success; on any error it prints sma_last_error() and exits 1.
+ * stream and prints z[0..3] and the replica-kernel time; with a fourth
+ * argument it also writes all d floats of z (raw little-endian fp32) there.
+ * Exit code 0 on success; on any error it prints sma_last_error() and exits 1.
  */
 #include <stdio.h>
 #include <stdlib.h>
@@ -42,6 +43,14 @@ int main(int argc, char** argv) {
   printf("abi=%d d=%lld k=%d rounds=%d z[0..3]=%.9g %.9g %.9g %.9g replica_kernel_ms=%.4f launches=%lld\n",
          sma_abi_version(), (long long)d, k, rounds, z[0], z[1], z[2], z[3], n ? ms / n : 0.0,
          (long long)sma_launch_count(h));
+  if (argc > 4) {
+    FILE* f = fopen(argv[4], "wb");
+    if (!f || fwrite(z, sizeof(float), (size_t)d, f) != (size_t)d) {
+      fprintf(stderr, "cannot write %s\n", argv[4]);
+      return 1;
+    }
+    fclose(f);
+  }
   sma_destroy(h);
   free(w0);
   free(z);

@@ -205,6 +205,11 @@ sma_status sma_synth_grads(sma_handle* h, int64_t round, uint64_t seed, void* cu
  *   a3 c_j = alpha (w_j - z) against the same z for all j   (line 9)
  *   a4 w_j <- w_j - gamma g_j - c_j, in place               (line 10)
  *   a5 per-GPU partial of sum_j c_j
+ *      (summation order, R7: any order is correct.  The full-grid kernel
+ *      adds the local c_j in ascending j; the small-round split kernel (chosen by
+ *      d_pad/4, r and the SMA_SPLIT_* knobs) adds them per lane group j mod G and
+ *      combines the G groups with xor-shuffles.  So results are bitwise stable
+ *      for a given (d, r, knobs) but may differ in the last bits across them.)
  *   a6 NCCL reduce-scatter of the partials (world > 1)
  *   a7 z <- z + sum c + mu (z - z_prev) on this GPU's shard (line 13)
  *   a8 NCCL all-gather of z (world > 1)
@@ -226,7 +231,12 @@ sma_status sma_step_local(sma_handle* h, void* cuda_stream);
 /* Alg. 2, one pass of its loop body over m GPUs (host only):
  *   if t[g] - t_prev[g] > tau: l[g] += 1;  else if t[g] < t_prev[g] and l[g] > 0:
  *   l[g] -= 1;  t_prev[g] = t[g].   (Initialise l = 1, t_prev = 0, lines 1-2.)
- * t: observed learning throughput per GPU (e.g. learner batches/s). */
+ * t: observed learning throughput per GPU (e.g. learner batches/s).
+ * Follows the paper literally, so l[g] may reach 0.  Before feeding l into
+ * sma_set_local_replicas the caller must (a) clamp it to >= 1 for a single-GPU
+ * handle (which rejects 0) and to the learner's n_samples / (world * batch), and
+ * (b) agree on ONE count across ranks (the resize takes a uniform l, R19),
+ * e.g. the minimum or rank 0's value broadcast over the process group. */
 sma_status sma_autotune_step(int32_t m, double tau, const double* t, int32_t* l, double* t_prev);
 
 /* Set the number of learners on EVERY GPU to l_new (the same count on all
@@ -236,8 +246,9 @@ sma_status sma_autotune_step(int32_t m, double tau, const double* t, int32_t* l,
  * (use sma_set_hparams, e.g. alpha = 1/k).  Gradients registered for kept
  * learners stay registered; added learners need one.  Synchronises; COLLECTIVE
  * when world > 1 (every rank calls it with the same l_new).
- * Errors: INVALID_ARG (l_new outside [0, SMA_MAX_LOCAL_REPLICAS], or 0 on a
- * single-GPU handle), CUDA, OOM. */
+ * Errors: INVALID_ARG (l_new outside [0, SMA_MAX_LOCAL_REPLICAS], 0 on a
+ * single-GPU handle, or -- with a learner attached -- l_new * world * batch >
+ * n_samples, which leaves no full round per epoch), CUDA, OOM. */
 sma_status sma_set_local_replicas(sma_handle* h, int32_t l_new, void* cuda_stream);
 
 /* ----------------------------------------------------------------- outputs */

@@ -171,7 +171,8 @@ struct P2PArgs {
   int64_t off4, len4;    // this rank's shard in float4 chunks
   float alpha, mu, coef_b;
   int n, rank;
-  unsigned* ctl;         // local: [0] barrier-A target, [1] barrier-B target, [2] CTA counter
+  unsigned* ctl;         // local: [0] barrier-A target, [1] barrier-B target, [2] CTA counter,
+                         // [3] barrier A passed (device-scope flag set by CTA 0)
   int* nonfinite;
   int push;              // SMA_FLAG_P2P_PUSH: the partials are already in local slots
 };

@@ -14,14 +14,20 @@
 // (release stores of a per-source flag into every peer's flag array, acquire
 // spins on the local array; targets kept in device memory so CUDA graphs can
 // replay the kernel) order "every partial is complete" before the loads and
-// "every shard has landed" before the next round.  A barrier that does not
-// complete within ~30 s traps, so a broken peer fails the process loudly.
+// "every shard has landed" before the next round.  Barrier A is taken at
+// system scope by ONE thread (CTA 0), which then releases the rest of the
+// grid through a device-scope flag in local memory: the other CTAs spin on an
+// L2-resident ld.acquire.gpu instead of n system-scope acquires each (the
+// release -> acquire chain is transitive, so every CTA's later loads of the
+// peers' partials are ordered after the peers' writes).  A barrier that does
+// not complete within ~30 s traps, so a broken peer fails the process loudly.
 //
 // Because no NCCL communicator is involved, several processes may share one
 // GPU (cudaIpc works within a device), which is how the multi-rank path is
 // tested on a single B200 (tests/test_p2p_multiprocess.py).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "sma_internal.h"
 
@@ -37,6 +43,14 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 // Wait until flags[0..n) (written by the n ranks) all reached `target`.
 __device__ __forceinline__ void wait_all(const unsigned* flags, int n, unsigned target) {
   const long long t0 = clock64();
@@ -46,11 +60,16 @@ __device__ __forceinline__ void wait_all(const unsigned* flags, int n, unsigned 
       __nanosleep(64);
     }
 }
-// Partials and z[cur] are read-only for the whole kernel on every rank, so the
-// non-coherent path is legal for them (no L1 allocation: peer data is never
-// reused); z[1-cur] of this rank's chunk is read then written by the same
-// thread, so it uses the coherent path.  (.cg loads here measured ~half the
-// bandwidth at n = 1.)
+// z[cur] is read-only for the whole kernel on every rank (its last writer is
+// the previous round's z-sync, complete before this launch), so the
+// non-coherent path is legal for it.  The partials are NOT: a peer's replica
+// kernel (Mode A), or its push epilogue (SMA_FLAG_P2P_PUSH, into this rank's
+// slots), may still be writing them while this kernel is already resident and
+// spinning at barrier A, and PTX requires .nc data to be read-only for the
+// kernel's whole lifetime.  They are loaded with weak coherent loads after the
+// barrier (ordered by its acquire + bar.sync), no L1 allocation: peer data is
+// never reused.  z[1-cur] of this rank's chunk is read then written by the same
+// thread (coherent path).  (.cg loads here measured ~half the bandwidth at n = 1.)
 __device__ __forceinline__ float4 ld_ro4(const float* p) {
   float4 v;
   asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
@@ -88,16 +107,29 @@ __device__ __forceinline__ float4 shard_update(float4 zc, float4 s, float4 zp, c
   return zn;
 }
 
-template <int MODE>
+// BAR = 1: barrier A at system scope in CTA 0 only, the grid released through
+// the device-scope flag ctl[3]; BAR = 0 (SMA_P2P_BARRIER=0, measurement only):
+// every CTA's thread 0 takes the n system-scope acquires itself (round 1).
+template <int MODE, int BAR>
 __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a) {
   __shared__ unsigned s_targetA;
   const int n = a.n;
   if (threadIdx.x == 0) {
     const unsigned tA = a.ctl[0] + 1u;
-    if (blockIdx.x == 0)  // barrier A: my partial is complete -> tell every rank
+    if (blockIdx.x == 0) {  // barrier A: my partial is complete -> tell every rank
       for (int g = 0; g < n; ++g)
         st_release_sys(reinterpret_cast<unsigned*>(a.base[g] + a.off_flags) + a.rank, tA);
-    wait_all(reinterpret_cast<const unsigned*>(a.base[a.rank] + a.off_flags), n, tA);
+      wait_all(reinterpret_cast<const unsigned*>(a.base[a.rank] + a.off_flags), n, tA);
+      if (BAR) st_release_gpu(a.ctl + 3, tA);  // every rank's partial is complete
+    } else if (BAR) {
+      const long long t0 = clock64();
+      while ((int)(ld_acquire_gpu(a.ctl + 3) - tA) < 0) {
+        if (clock64() - t0 > 60000000000ll) __trap();
+        __nanosleep(32);
+      }
+    } else {
+      wait_all(reinterpret_cast<const unsigned*>(a.base[a.rank] + a.off_flags), n, tA);
+    }
     s_targetA = tA;
   }
   __syncthreads();
@@ -120,7 +152,7 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
     const int64_t e0 = (a.off4 + c) << 2, e1 = (a.off4 + c + stride) << 2;
     float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0;
     for (int g = 0; g < n; ++g) {  // a6: the shard's sum over ranks, ascending rank
-      const float4 v0 = ld_ro4(part_ptr(g, e0)), v1 = ld_ro4(part_ptr(g, e1));
+      const float4 v0 = ld_rw4(part_ptr(g, e0)), v1 = ld_rw4(part_ptr(g, e1));
       s0.x = __fadd_rn(s0.x, v0.x); s0.y = __fadd_rn(s0.y, v0.y);
       s0.z = __fadd_rn(s0.z, v0.z); s0.w = __fadd_rn(s0.w, v0.w);
       s1.x = __fadd_rn(s1.x, v1.x); s1.y = __fadd_rn(s1.y, v1.y);
@@ -140,7 +172,7 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
     const int64_t e = (a.off4 + c) << 2;  // element offset in the padded vector
     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int g = 0; g < n; ++g) {
-      const float4 v = ld_ro4(part_ptr(g, e));
+      const float4 v = ld_rw4(part_ptr(g, e));
       sum.x = __fadd_rn(sum.x, v.x); sum.y = __fadd_rn(sum.y, v.y);
       sum.z = __fadd_rn(sum.z, v.z); sum.w = __fadd_rn(sum.w, v.w);
     }
@@ -178,10 +210,17 @@ cudaError_t launch_zsync_p2p(int mode, const P2PArgs& a, int num_ctas, cudaStrea
   // Launched without PDL (no measurable gain on one GPU: C3 Mode A 41-46k rounds/s
   // either way, within the run-to-run spread of the barrier spin; profiles/r01_pdl.txt),
   // so the next replica kernel starts only after this kernel has completed.
-  if (mode == kPartialA)
-    zsync_p2p_kernel<kPartialA><<<grid, kP2PThreads, 0, s>>>(a);
-  else
-    zsync_p2p_kernel<kPartialB><<<grid, kP2PThreads, 0, s>>>(a);
+  static const int bar = [] {
+    const char* e = getenv("SMA_P2P_BARRIER");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  if (mode == kPartialA) {
+    if (bar) zsync_p2p_kernel<kPartialA, 1><<<grid, kP2PThreads, 0, s>>>(a);
+    else zsync_p2p_kernel<kPartialA, 0><<<grid, kP2PThreads, 0, s>>>(a);
+  } else {
+    if (bar) zsync_p2p_kernel<kPartialB, 1><<<grid, kP2PThreads, 0, s>>>(a);
+    else zsync_p2p_kernel<kPartialB, 0><<<grid, kP2PThreads, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 

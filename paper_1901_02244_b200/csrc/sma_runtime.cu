@@ -850,6 +850,10 @@ sma_status sma_set_local_replicas(sma_handle* h, int32_t l_new, void* stream) {
     return fail(SMA_ERR_INVALID_ARG, "l_new=%d outside [0, %d]", l_new, SMA_MAX_LOCAL_REPLICAS);
   if (!h->collective && l_new == 0)
     return fail(SMA_ERR_INVALID_ARG, "a single-GPU handle needs at least one replica");
+  if (h->learner && (int64_t)l_new * h->cfg.world * h->batch > h->n_samples)
+    return fail(SMA_ERR_INVALID_ARG,
+                "l_new=%d: %d learners x batch %d exceed the attached learner's %lld samples",
+                l_new, l_new * h->cfg.world, h->batch, (long long)h->n_samples);
   DeviceGuard guard(h->dev);
   cudaStream_t s = (cudaStream_t)stream;
   STATUS_TRY(sync_handle(h));
@@ -1055,11 +1059,23 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
                 (long long)h->cfg.d, (long long)dl);
   if (n_samples < (int64_t)h->cfg.k * batch || n_samples > INT32_MAX)
     return fail(SMA_ERR_INVALID_ARG, "n_samples must be in [k*batch, 2^31)");
-  const size_t smem_need =
-      kind == 0 ? sizeof(float) * ((size_t)in_dim + (size_t)batch * (64 + classes))
-                : sizeof(float) * ((size_t)(batch + 16) * in_dim);
+  // dynamic shared memory of every learner kernel (sma_kernels.cu, sma_learner_mlp.cu):
+  // softmax logits + dW slice; MLP layer 1 (batch rows + up to 16 W1 rows), logits
+  // (h row + W2 + b2), head (h, W2, e, staged a1 as float2)
+  size_t smem_need = 0;
+  if (kind == 0) {
+    smem_need = sizeof(float) * ((size_t)in_dim + (size_t)batch * (64 + classes));
+  } else {
+    const size_t hd = (size_t)hidden, b = (size_t)batch, c = (size_t)classes;
+    const size_t sm1 = sizeof(float) * ((b + 16) * (size_t)in_dim);
+    const size_t smL = sizeof(float) * (hd + c * hd + c);
+    const size_t sm2 = sizeof(float) * (b * hd + c * hd + b * c) + 16 + sizeof(float) * 2 * b * hd;
+    smem_need = sm1 > smL ? sm1 : smL;
+    if (sm2 > smem_need) smem_need = sm2;
+  }
   if (smem_need > 200 * 1024)
-    return fail(SMA_ERR_INVALID_ARG, "batch/in_dim too large for the learner's shared memory");
+    return fail(SMA_ERR_INVALID_ARG,
+                "learner shapes need %zu B of shared memory in one kernel (limit 200 KB)", smem_need);
   DeviceGuard guard(h->dev);
   STATUS_TRY(sync_handle(h));
   for (int i = 0; i < 2; ++i) {
@@ -1114,6 +1130,9 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
 static sma_status learner_batch(sma_handle* h, int64_t round, cudaStream_t s, int* buf_out,
                          int64_t* pos0_out) {
   const int64_t E = h->n_samples / ((int64_t)h->cfg.k * h->batch);
+  if (E < 1)  // as sma_plan_batch_indices: k learners need k * batch samples per round
+    return fail(SMA_ERR_INVALID_ARG, "n_samples=%lld < k*batch=%lld: no full round per epoch",
+                (long long)h->n_samples, (long long)h->cfg.k * h->batch);
   const int64_t e = round / E;
   const int buf = (int)(e & 1);
   if (h->perm_epoch[buf] != e) {

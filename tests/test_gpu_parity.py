@@ -474,35 +474,102 @@ def test_mlp_gradient_single_round(torch_cuda, S, orc):
     h.close()
 
 
+MLP_W1 = 256 * 784
+
+
+def mlp_relu_decisions_agree(Wg, Wo, X, rows):
+    """R18's precondition for MLP parity, measured directly: the ReLU mask is an
+    integer decision, and the GPU takes it on its own fp32 state W_gpu (at
+    fp64-level accuracy: fp32 dot + a-priori bound, Dot2 where uncertain) while
+    the oracle takes it on its fp64 state.  Parity at 1e-5 is expected exactly
+    when every decision [a > 0] agrees.  Returns (agree, max |a_gpu - a_orc|
+    (the fp32-vs-fp64 state drift seen through the pre-activations), min |a_orc|
+    (the oracle's distance to a kink)), all in fp64."""
+    xr = X[rows].astype(np.float64)
+    ag = Wg[:MLP_W1].astype(np.float64).reshape(256, 784) @ xr.T + \
+        Wg[MLP_W1:MLP_W1 + 256].astype(np.float64)[:, None]
+    ao = Wo[:MLP_W1].reshape(256, 784) @ xr.T + Wo[MLP_W1:MLP_W1 + 256][:, None]
+    return bool(np.all((ag > 0) == (ao > 0))), float(np.max(np.abs(ag - ao))), \
+        float(np.min(np.abs(ao)))
+
+
+def mlp_sma_vs_oracle(torch, S, orc, X, y, k, b, seed, a, g, m, R, w0, flags=0,
+                      step=None):
+    """R rounds of SMA with the MLP learner in the loop on the GPU (step(h, i);
+    default sma_learner_step) and in the oracle, in lockstep.  Before every
+    round the GPU replicas are read back and the ReLU decisions of every
+    learner's batch are checked against the oracle's (the precondition under
+    which fp32 parity holds, R18).  Returns (handle, oracle state, stats)."""
+    h = S.Sma(MLP_D, k, a, g, m, w0, flags=flags)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    S.sma_learner_attach(h.h, 1, 784, 256, 10, b, Xd, yd, X.shape[0], seed)
+    h._keep = (Xd, yd)
+    st = orc.State.init(w0.astype(np.float64), k)
+    s = torch.cuda.Stream()
+    step = step or (lambda hh, i: S.sma_learner_step(hh.h, i, s))
+    drift, margin, disagree = 0.0, np.inf, []
+    for i in range(R):
+        s.synchronize()
+        G = []
+        for j in range(k):
+            rows = orc.batch_indices(X.shape[0], k, b, seed, i, j)
+            ok, dr, mg = mlp_relu_decisions_agree(h.replica(j), st.W[j], X, rows)
+            drift, margin = max(drift, dr), min(margin, mg)
+            if not ok:
+                disagree.append((i, j))
+            G.append(orc.mlp_loss_grad(X, y, rows, st.W[j])[1])
+        step(h, i)
+        st.round(np.stack(G), a, g, m)
+    s.synchronize()
+    stats = dict(k=k, b=b, rounds=R, max_preact_drift=drift, min_oracle_margin=margin,
+                 disagreements=disagree)
+    print("MLP-PARITY", stats)
+    return h, st, stats
+
+
 def test_mlp_learner_sma_parity(torch_cuda, S, orc):
     """SMA with the MLP learner in the loop (k = 2, b = 8, 30 rounds) vs the fp64
-    oracle.  Parity is conditioned on no pre-activation coming within the
-    fp32-vs-fp64 state divergence of a ReLU kink (the mask is an integer
-    decision, R18); the oracle's margin is asserted every round."""
+    oracle, through sma_learner_grads + sma_step.  Precondition (R18), measured
+    every round: every ReLU decision at the GPU's fp32 state equals the
+    oracle's at its fp64 state."""
     torch = torch_cuda
     X, y = sma_inputs.blobs(4_000, seed=13)
     k, b, R = 2, 8, 30
     a, g, m = F32(1 / k), F32(0.05), F32(0.9)
     w0 = np.random.default_rng(6).normal(0, 0.05, MLP_D).astype(np.float32)
-    h = S.Sma(MLP_D, k, a, g, m, w0)
-    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
-    S.sma_learner_attach(h.h, 1, 784, 256, 10, b, Xd, yd, X.shape[0], 33)
-    st = orc.State.init(w0.astype(np.float64), k)
-    min_margin = np.inf
-    for i in range(R):
-        S.sma_learner_grads(h.h, i, torch.cuda.current_stream())
-        h.step()
-        G = []
-        for j in range(k):
-            rows = orc.batch_indices(X.shape[0], k, b, 33, i, j)
-            _, gj, mg = orc.mlp_loss_grad(X, y, rows, st.W[j])
-            G.append(gj)
-            min_margin = min(min_margin, mg)
-        st.round(np.stack(G), a, g, m)
-    assert min_margin > 5e-6, f"batch too close to a ReLU kink for fp32 parity: {min_margin}"
+
+    def step(hh, i):
+        S.sma_learner_grads(hh.h, i, torch.cuda.current_stream())
+        hh.step()
+    h, st, stats = mlp_sma_vs_oracle(torch, S, orc, X, y, k, b, 33, a, g, m, R, w0, step=step)
+    assert not stats["disagreements"], stats
     assert relerr(h.central(), st.z) <= TOL
     for j in range(k):
         assert relerr(h.replica(j), st.W[j]) <= TOL
+    h.close()
+
+
+@pytest.mark.parametrize("k", [4, 16, 12, 32])
+def test_mlp_bench_configs_100_rounds(torch_cuda, S, orc, k):
+    """The MLP bench configuration (`bench.py --config MLP --k K`): 784-256-10,
+    b = 16, alpha = 1/k, gamma = 0.1, mu = 0.9, w0 ~ N(0, 0.05) (seed 6),
+    60,000 MNIST-shaped blobs (seed 4), batch seed 99, sma_learner_step, 100
+    rounds vs the fp64 oracle at <= 1e-5 (north_star) on z, z_prev and every
+    replica.  The default learner policy puts layer 1 on the SIMT kernel at
+    k = 4 and 16 and on tcgen05 (3xTF32) at k = 12 and 32.
+    Precondition (R18), measured every round on every learner's batch: the
+    ReLU decisions at the GPU's fp32 state equal the oracle's."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(60_000, seed=4)
+    b, R = 16, 100
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    w0 = np.random.default_rng(6).normal(0, 0.05, MLP_D).astype(np.float32)
+    h, st, stats = mlp_sma_vs_oracle(torch, S, orc, X, y, k, b, 99, a, g, m, R, w0)
+    assert not stats["disagreements"], stats
+    assert relerr(h.central(), st.z) <= TOL, stats
+    assert relerr(h.central_prev(), st.z_prev) <= TOL, stats
+    for j in range(k):
+        assert relerr(h.replica(j), st.W[j]) <= TOL, (j, stats)
     h.close()
 
 
@@ -524,11 +591,11 @@ def test_paper_config_sizes_sampled_parity(torch_cuda, S, orc, cfg):
     h.close()
 
 
-def test_learner_step_fused_is_bitwise_unfused(torch_cuda, S, orc):
-    """sma_learner_step's fused softmax round == sma_learner_grads + sma_step
-    over 60 rounds crossing an epoch (bit for bit when the unfused replica kernel
-    sums the corrections in the same order; the small-round split kernel sums
-    them per lane group, so here to 1e-6), and both match the oracle (C1 shape)."""
+def test_learner_step_fused_matches_unfused(torch_cuda, S, orc):
+    """sma_learner_step's fused softmax round vs sma_learner_grads + sma_step
+    over 60 rounds crossing an epoch, to 1e-6 (not bitwise: the fused kernel sums
+    the corrections in ascending j, the unfused small-round split kernel per lane
+    group, R7), and both match the oracle (C1 shape)."""
     torch = torch_cuda
     X, y = sma_inputs.blobs(3_000, seed=4)
     k, b, R = 4, 16, 60
@@ -651,7 +718,8 @@ def test_learner_step_overlapped_zsync(torch_cuda, S, orc, kind, variant):
     kernels of round i (GlobalSync || Learning, fig:dependencies f):
     the same arithmetic as sma_learner_grads + sma_step, so bitwise equal to it
     over 40 rounds crossing an epoch, and within tolerance of the oracle
-    (softmax: C1 shape; MLP: 784-256-10, margin-conditioned as R18)."""
+    (softmax: C1 shape; MLP: 784-256-10, with R18's precondition -- equal ReLU decisions at
+    the GPU and oracle states -- checked every round)."""
     torch = torch_cuda
     X, y = sma_inputs.blobs(3_000, seed=4 if kind == 0 else 13)
     d = 7850 if kind == 0 else MLP_D
@@ -660,18 +728,27 @@ def test_learner_step_overlapped_zsync(torch_cuda, S, orc, kind, variant):
     w0 = np.zeros(d, np.float32) if kind == 0 else \
         np.random.default_rng(6).normal(0, 0.05, d).astype(np.float32)
     Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
-    hs = []
+    hs, ss = [], []
     for overlapped in (True, False):
         h = S.Sma(d, k, a, g, m, w0, flags=COLLECTIVE_FLAGS[variant])
         S.sma_learner_attach(h.h, kind, 784, 256 if kind else 0, 10, b, Xd, yd, X.shape[0], 99)
-        s = torch.cuda.Stream()
-        for i in range(R):
-            if overlapped:
-                S.sma_learner_step(h.h, i, s)
-            else:
-                S.sma_learner_grads(h.h, i, s)
-                h.step(s)
         hs.append(h)
+        ss.append(torch.cuda.Stream())
+    st = orc.State.init(w0.astype(np.float64), k)
+    disagree = []
+    for i in range(R):
+        if kind == 1:   # R18 precondition, measured: ReLU decisions at the GPU state == oracle's
+            ss[1].synchronize()
+            G = []
+            for j in range(k):
+                rows = orc.batch_indices(X.shape[0], k, b, 99, i, j)
+                if not mlp_relu_decisions_agree(hs[1].replica(j), st.W[j], X, rows)[0]:
+                    disagree.append((i, j))
+                G.append(orc.mlp_loss_grad(X, y, rows, st.W[j])[1])
+            st.round(np.stack(G), a, g, m)
+        S.sma_learner_step(hs[0].h, i, ss[0])
+        S.sma_learner_grads(hs[1].h, i, ss[1])
+        hs[1].step(ss[1])
     assert np.array_equal(hs[0].central(), hs[1].central())
     assert np.array_equal(hs[0].central_prev(), hs[1].central_prev())
     for j in range(k):
@@ -680,18 +757,10 @@ def test_learner_step_overlapped_zsync(torch_cuda, S, orc, kind, variant):
         zr, _, _ = orc.run_softmax(X, y, b, 99, k, a, g, m, R, w0.astype(np.float64))
         assert relerr(hs[0].central(), zr) <= TOL
     else:
-        st = orc.State.init(w0.astype(np.float64), k)
-        mm = np.inf
-        for i in range(R):
-            G = []
-            for j in range(k):
-                _, gj, mg = orc.mlp_loss_grad(X, y, orc.batch_indices(X.shape[0], k, b, 99, i, j),
-                                              st.W[j])
-                G.append(gj)
-                mm = min(mm, mg)
-            st.round(np.stack(G), a, g, m)
-        if mm > 5e-6:
-            assert relerr(hs[0].central(), st.z) <= TOL
+        assert not disagree, disagree
+        assert relerr(hs[0].central(), st.z) <= TOL
+        for j in range(k):
+            assert relerr(hs[0].replica(j), st.W[j]) <= TOL
     for h in hs:
         h.close()
 
