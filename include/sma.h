@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define SMA_ABI_VERSION 1
+#define SMA_ABI_VERSION 2
 #define SMA_MAX_LOCAL_REPLICAS 64   /* r = replicas per GPU, P:1193-1194 ("m") */
 #define SMA_NCCL_ID_BYTES 128
 #define SMA_P2P_HANDLE_BYTES 64  /* cudaIpcMemHandle_t */
@@ -192,6 +192,19 @@ sma_status sma_set_learner_grads(sma_handle* h, int32_t j, const float* g_dev);
 sma_status sma_set_learner_grads_host(sma_handle* h, int32_t j, const float* g_host,
                                       void* cuda_stream);
 
+/* Pipelined host intake (the end-to-end path of a training loop that streams
+ * one batch of gradients per round from the host).  Copies the RAW gradients
+ * of ALL r local learners -- g_host[i] is learner local_first + i, d floats,
+ * pinned host memory for an asynchronous copy -- into the handle's internal
+ * gradient set `set` (0 or 1; two sets so the copies for round s+1 overlap
+ * round s) on the handle's own host-to-device stream, ordered after the last
+ * round that read that set, and registers them (replacing any registration)
+ * for the next sma_step / sma_step_local, which waits for the copies on its
+ * stream.  Does not block the host; g_host must stay valid until the copies
+ * have completed (sma_synchronize).  Errors: INVALID_ARG (set not 0/1, NULL
+ * pointer), CUDA, OOM. */
+sma_status sma_stage_grads_host(sma_handle* h, int32_t set, const float* const* g_host);
+
 /* Fill the handle's gradient buffers of all LOCAL learners with the synthetic
  * raw gradients of round `round` (R9):
  *   g_j^i[p] = (U(seed, (i k + j) d + p) - 1/2) 2^-4,
@@ -258,6 +271,20 @@ sma_status sma_set_local_replicas(sma_handle* h, int32_t l_new, void* cuda_strea
  * Synchronises the host with all work the handle has enqueued.  Every rank
  * holds the full z.  Errors: INVALID_ARG, CUDA, NONFINITE (CHECK_FINITE). */
 sma_status sma_get_central(sma_handle* h, float* z_out, int out_is_device);
+
+/* Asynchronous read-back of z for the end-to-end path: enqueue a copy of the
+ * central model as of every round enqueued so far (d floats) into z_host
+ * (pinned host memory) on the handle's device-to-host stream, after those
+ * rounds.  Does not block the host.  The round that would overwrite that z
+ * buffer (z and z_prev are ping-ponged, so the second sma_step from now) waits
+ * for the copy on its stream, so the value read is exact.  Completion:
+ * sma_synchronize.  Errors: INVALID_ARG, CUDA. */
+sma_status sma_get_central_async(sma_handle* h, float* z_host);
+
+/* Block the host until all work the handle has enqueued -- rounds, staged
+ * host-to-device copies and asynchronous read-backs -- has completed.
+ * Errors: CUDA, NONFINITE (CHECK_FINITE). */
+sma_status sma_synchronize(sma_handle* h);
 
 /* Same for z_prev (the central model at the beginning of the previous round,
  * P:630-631), needed to checkpoint/resume without losing momentum. */

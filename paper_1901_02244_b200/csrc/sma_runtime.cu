@@ -93,6 +93,17 @@ struct sma_handle {
   const float* gptr[SMA_MAX_LOCAL_REPLICAS] = {};
   uint64_t ver = 1;  // bumps when anything baked into a graph changes
 
+  // pipelined host intake and asynchronous read-back (sma_stage_grads_host,
+  // sma_get_central_async): two internal gradient sets G2[2][r][d_pad] filled on
+  // sH2D, z copied out on sD2H; events order each against the rounds
+  float* G2 = nullptr;
+  cudaStream_t sH2D = nullptr, sD2H = nullptr;
+  cudaEvent_t evStaged[2] = {}, evUsed[2] = {}, evZread[2] = {}, evAsync = nullptr;
+  bool used_rec[2] = {false, false}, zread_pending[2] = {false, false};
+  bool async_pending = false, h2d_pending = false;
+  int cur_set = -1;        // the gradient set the registrations point into (-1: none)
+  bool stage_wait = false; // the next round must wait for evStaged[cur_set]
+
   ncclComm_t comm = nullptr;
   // collective buffers from ncclMemAlloc (NVLS-capable) and their registrations
   std::vector<void*> nccl_allocs, nccl_regs;
@@ -128,6 +139,8 @@ struct sma_handle {
   float2* mlp_A1 = nullptr;  // MLP scratch, sized for SMA_MAX_LOCAL_REPLICAS learners
   float* mlp_DA = nullptr;
   float* mlp_E = nullptr;
+  float* mlp_PL = nullptr;     // fused MLP round: partial logits [num_sms][16][32]
+  unsigned* mlp_bar = nullptr; // fused MLP round: grid barrier state [2]
   const float* X = nullptr;
   const int32_t* y = nullptr;
   int64_t n_samples = 0;
@@ -210,6 +223,15 @@ void free_all(sma_handle* h) {
   if (h->evDone) cudaEventDestroy(h->evDone);
   if (h->sB) cudaStreamDestroy(h->sB);
   if (h->sIO) cudaStreamDestroy(h->sIO);
+  if (h->sH2D) cudaStreamDestroy(h->sH2D);
+  if (h->sD2H) cudaStreamDestroy(h->sD2H);
+  for (int i = 0; i < 2; ++i) {
+    if (h->evStaged[i]) cudaEventDestroy(h->evStaged[i]);
+    if (h->evUsed[i]) cudaEventDestroy(h->evUsed[i]);
+    if (h->evZread[i]) cudaEventDestroy(h->evZread[i]);
+  }
+  if (h->evAsync) cudaEventDestroy(h->evAsync);
+  cudaFree(h->G2);
   cudaFree(h->W);
   cudaFree(h->zbuf);
   cudaFree(h->P);
@@ -224,6 +246,8 @@ void free_all(sma_handle* h) {
   cudaFree(h->mlp_A1);
   cudaFree(h->mlp_DA);
   cudaFree(h->mlp_E);
+  cudaFree(h->mlp_PL);
+  cudaFree(h->mlp_bar);
   if (h->perm_next.valid()) h->perm_next.wait();
   for (int i = 0; i < 2; ++i) {
     if (h->perm_host[i]) cudaFreeHost(h->perm_host[i]);
@@ -246,15 +270,54 @@ void set_gptr(sma_handle* h, int slot, const float* p) {
   }
 }
 
+// A registration from any path but sma_stage_grads_host leaves the staged set.
+void leave_staged_set(sma_handle* h) {
+  h->cur_set = -1;
+  h->stage_wait = false;
+}
+
 sma_status mark_done(sma_handle* h, cudaStream_t s) {
   CUDA_TRY(cudaEventRecord(h->evDone, s));
   h->any_work = true;
   return SMA_OK;
 }
 
-// Wait for everything the handle enqueued, on the host.
+// Wait for everything the handle enqueued, on the host (rounds, staged
+// host-to-device copies, asynchronous read-backs).
 sma_status sync_handle(sma_handle* h) {
   if (h->any_work) CUDA_TRY(cudaEventSynchronize(h->evDone));
+  if (h->h2d_pending) {
+    CUDA_TRY(cudaStreamSynchronize(h->sH2D));
+    h->h2d_pending = false;
+  }
+  if (h->async_pending) {
+    CUDA_TRY(cudaEventSynchronize(h->evAsync));
+    h->async_pending = false;
+  }
+  return SMA_OK;
+}
+
+// Cross-stream ordering of a round enqueued on s with the pipelined intake and
+// read-back: wait for the staged gradient copies it reads, and -- if it writes
+// the z_prev half (writes_z) -- for an asynchronous read-back of the z value
+// that half still holds; afterwards, mark the gradient set as read by s.
+sma_status pre_round(sma_handle* h, cudaStream_t s, bool writes_z) {
+  if (h->stage_wait) {
+    CUDA_TRY(cudaStreamWaitEvent(s, h->evStaged[h->cur_set], 0));
+    h->stage_wait = false;
+  }
+  const int b = 1 - h->cur;
+  if (writes_z && h->zread_pending[b]) {
+    CUDA_TRY(cudaStreamWaitEvent(s, h->evZread[b], 0));
+    h->zread_pending[b] = false;
+  }
+  return SMA_OK;
+}
+sma_status post_round(sma_handle* h, cudaStream_t s) {
+  if (h->cur_set >= 0) {
+    CUDA_TRY(cudaEventRecord(h->evUsed[h->cur_set], s));
+    h->used_rec[h->cur_set] = true;
+  }
   return SMA_OK;
 }
 
@@ -740,6 +803,7 @@ sma_status sma_set_learner_grads(sma_handle* h, int32_t j, const float* g_dev) {
   if (!g_dev || (reinterpret_cast<uintptr_t>(g_dev) & 15u))
     return fail(SMA_ERR_INVALID_ARG, "gradient pointer must be non-NULL and 16-byte aligned");
   set_gptr(h, slot, g_dev);
+  leave_staged_set(h);
   return SMA_OK;
 }
 
@@ -754,7 +818,65 @@ sma_status sma_set_learner_grads_host(sma_handle* h, int32_t j, const float* g_h
   float* dst = h->G + (int64_t)slot * h->d_pad;
   CUDA_TRY(cudaMemcpyAsync(dst, g_host, sizeof(float) * h->cfg.d, cudaMemcpyHostToDevice, s));
   set_gptr(h, slot, dst);
+  leave_staged_set(h);
   return mark_done(h, s);
+}
+
+sma_status sma_stage_grads_host(sma_handle* h, int32_t set, const float* const* g_host) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (set != 0 && set != 1) return fail(SMA_ERR_INVALID_ARG, "gradient set %d (0 or 1)", set);
+  if (!g_host && h->r > 0) return fail(SMA_ERR_INVALID_ARG, "NULL pointer array");
+  for (int i = 0; i < h->r; ++i)
+    if (!g_host[i]) return fail(SMA_ERR_INVALID_ARG, "NULL gradient of local learner %d", i);
+  if (h->r == 0) return SMA_OK;
+  DeviceGuard guard(h->dev);
+  const size_t dp = (size_t)h->d_pad;
+  if (!h->G2) {
+    CUDA_TRY(cudaMalloc(&h->G2, sizeof(float) * 2 * dp * (size_t)h->r));
+    CUDA_TRY(cudaMemset(h->G2, 0, sizeof(float) * 2 * dp * (size_t)h->r));  // padding stays 0
+  }
+  if (!h->sH2D) CUDA_TRY(cudaStreamCreateWithFlags(&h->sH2D, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    if (!h->evStaged[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->evStaged[i], cudaEventDisableTiming));
+    if (!h->evUsed[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->evUsed[i], cudaEventDisableTiming));
+  }
+  // the set is free again once the last round that read it has run
+  if (h->used_rec[set]) CUDA_TRY(cudaStreamWaitEvent(h->sH2D, h->evUsed[set], 0));
+  float* base = h->G2 + (size_t)set * dp * (size_t)h->r;
+  for (int i = 0; i < h->r; ++i) {
+    CUDA_TRY(cudaMemcpyAsync(base + (size_t)i * dp, g_host[i], sizeof(float) * h->cfg.d,
+                             cudaMemcpyHostToDevice, h->sH2D));
+    set_gptr(h, i, base + (size_t)i * dp);
+  }
+  CUDA_TRY(cudaEventRecord(h->evStaged[set], h->sH2D));
+  h->cur_set = set;
+  h->stage_wait = true;
+  h->h2d_pending = true;
+  return SMA_OK;
+}
+
+sma_status sma_get_central_async(sma_handle* h, float* z_host) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  if (!z_host) return fail(SMA_ERR_INVALID_ARG, "NULL output");
+  DeviceGuard guard(h->dev);
+  if (!h->sD2H) CUDA_TRY(cudaStreamCreateWithFlags(&h->sD2H, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i)
+    if (!h->evZread[i]) CUDA_TRY(cudaEventCreateWithFlags(&h->evZread[i], cudaEventDisableTiming));
+  if (!h->evAsync) CUDA_TRY(cudaEventCreateWithFlags(&h->evAsync, cudaEventDisableTiming));
+  if (h->any_work) CUDA_TRY(cudaStreamWaitEvent(h->sD2H, h->evDone, 0));
+  CUDA_TRY(cudaMemcpyAsync(z_host, h->z(), sizeof(float) * h->cfg.d, cudaMemcpyDeviceToHost, h->sD2H));
+  CUDA_TRY(cudaEventRecord(h->evZread[h->cur], h->sD2H));
+  h->zread_pending[h->cur] = true;
+  CUDA_TRY(cudaEventRecord(h->evAsync, h->sD2H));
+  h->async_pending = true;
+  return SMA_OK;
+}
+
+sma_status sma_synchronize(sma_handle* h) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  DeviceGuard guard(h->dev);
+  STATUS_TRY(sync_handle(h));
+  return check_nonfinite(h);
 }
 
 sma_status sma_synth_grads(sma_handle* h, int64_t round, uint64_t seed, void* stream) {
@@ -768,6 +890,7 @@ sma_status sma_synth_grads(sma_handle* h, int64_t round, uint64_t seed, void* st
                               h->num_sms, s));
   ++h->launches;
   for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
+  leave_staged_set(h);
   return mark_done(h, s);
 }
 
@@ -781,6 +904,7 @@ sma_status sma_step(sma_handle* h, void* stream) {
       return fail(SMA_ERR_GRADS_MISSING, "learner %d has no registered gradient", h->j0 + i);
   DeviceGuard guard(h->dev);
   cudaStream_t s = (cudaStream_t)stream;
+  STATUS_TRY(pre_round(h, s, true));
   if (h->overlap && h->q_dirty) STATUS_TRY(enqueue_q_prologue(h, s));
   if (h->graphs && !h->timing && s != nullptr) {
     const int key = h->cur;
@@ -812,6 +936,7 @@ sma_status sma_step(sma_handle* h, void* stream) {
   } else {
     STATUS_TRY(enqueue_round(h, s));
   }
+  STATUS_TRY(post_round(h, s));
   advance(h);
   return mark_done(h, s);
 }
@@ -825,6 +950,7 @@ sma_status sma_step_local(sma_handle* h, void* stream) {
   if (h->r == 0) return SMA_OK;
   DeviceGuard guard(h->dev);
   cudaStream_t s = (cudaStream_t)stream;
+  STATUS_TRY(pre_round(h, s, false));
   ReplicaArgs a{};
   a.W = h->W;
   a.ld = h->d_pad;
@@ -839,6 +965,7 @@ sma_status sma_step_local(sma_handle* h, void* stream) {
   if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
   CUDA_TRY(launch_replica_step(kLocal, false, a, h->num_sms, s));
   if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
+  STATUS_TRY(post_round(h, s));
   ++h->launches;
   h->q_dirty = true;  // Mode B: Q^i = sum_j (w_j - z_prev) must be recomputed
   return mark_done(h, s);
@@ -869,6 +996,13 @@ sma_status sma_set_local_replicas(sma_handle* h, int32_t l_new, void* stream) {
                                    h->num_sms, s));
   float* G2 = nullptr;
   float* C2 = nullptr;
+  float* S2 = nullptr;  // the two staged gradient sets, [2][l_new][d_pad]
+  if (h->G2) {
+    STATUS_TRY(alloc_zero(&S2, 2 * dp * (l_new > 0 ? l_new : 1)));
+    for (int set = 0; set < 2 && keep > 0; ++set)
+      CUDA_TRY(cudaMemcpyAsync(S2 + (size_t)set * dp * l_new, h->G2 + (size_t)set * dp * h->r,
+                               sizeof(float) * dp * keep, cudaMemcpyDeviceToDevice, s));
+  }
   if (h->G) {
     STATUS_TRY(alloc_zero(&G2, dp * (l_new > 0 ? l_new : 1)));
     if (keep > 0)
@@ -882,9 +1016,18 @@ sma_status sma_set_local_replicas(sma_handle* h, int32_t l_new, void* stream) {
     const float* old = h->gptr[i];
     if (h->G && old >= h->G && old < h->G + dp * h->r)
       gp[i] = G2 + (old - h->G);
-    else
+    else if (h->G2 && old >= h->G2 && old < h->G2 + 2 * dp * h->r) {
+      const size_t off = (size_t)(old - h->G2), set = off / (dp * h->r);
+      gp[i] = S2 + set * dp * l_new + (off - set * dp * h->r);
+    } else
       gp[i] = old;
   }
+  if (h->G2) {
+    cudaFree(h->G2);
+    h->G2 = S2;
+    h->used_rec[0] = h->used_rec[1] = false;  // the copy above synchronised the stream
+  }
+  if (l_new > keep) leave_staged_set(h);  // added learners need a fresh registration
   cudaFree(h->W);
   h->W = W2;
   if (h->G) {
@@ -1105,6 +1248,11 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
       cudaFree(h->mlp_E);
       h->mlp_E = nullptr;
       CUDA_TRY(cudaMalloc(&h->mlp_E, sizeof(float) * (size_t)SMA_MAX_LOCAL_REPLICAS * batch * classes));
+      if (!h->mlp_PL) CUDA_TRY(cudaMalloc(&h->mlp_PL, sizeof(float) * (size_t)h->num_sms * 16 * 32));
+      if (!h->mlp_bar) {
+        CUDA_TRY(cudaMalloc(&h->mlp_bar, 2 * sizeof(unsigned)));
+        CUDA_TRY(cudaMemset(h->mlp_bar, 0, 2 * sizeof(unsigned)));
+      }
     }
     CUDA_TRY(cudaMalloc(&h->mlp_DA, sizeof(float) * n));
   }
@@ -1181,12 +1329,25 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
                                  h->classes, h->W, h->d_pad, h->r, h->j0, h->mlp_DA, h->G, s));
     h->launches += 2;
   } else {
-    CUDA_TRY(launch_mlp_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim, h->hidden,
-                             h->classes, h->W, h->d_pad, h->r, h->j0, h->mlp_A1, h->mlp_E,
-                             h->mlp_DA, h->G, s));
-    h->launches += 4;
+    ReplicaArgs a{};
+    a.W = h->W;
+    a.ld = h->d_pad;
+    a.r = h->r;
+    cudaError_t e = launch_mlp_round(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim,
+                                     h->hidden, h->classes, h->j0, h->mlp_PL, h->mlp_bar, h->G, a,
+                                     false, h->num_sms, s);
+    if (e == cudaErrorNotSupported) {  // the five-kernel path
+      CUDA_TRY(launch_mlp_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim, h->hidden,
+                               h->classes, h->W, h->d_pad, h->r, h->j0, h->mlp_A1, h->mlp_E,
+                               h->mlp_DA, h->G, s));
+      h->launches += 4;
+    } else {
+      CUDA_TRY(e);
+      h->launches += 1;
+    }
   }
   for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
+  leave_staged_set(h);
   return mark_done(h, s);
 }
 
@@ -1213,11 +1374,52 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
       return fail(SMA_ERR_STATE, "SMA_FLAG_P2P_ZSYNC: call sma_p2p_connect on every rank first");
     DeviceGuard guard(h->dev);
     cudaStream_t s = (cudaStream_t)stream;
+    leave_staged_set(h);  // the learner writes the handle's own gradient buffers
+    STATUS_TRY(pre_round(h, s, true));
     if (h->q_dirty) STATUS_TRY(enqueue_q_prologue(h, s));
     const LearnerFn fn = [&](cudaStream_t ls) { return sma_learner_grads(h, round, ls); };
     STATUS_TRY(enqueue_round(h, s, &fn));
     advance(h);
     return mark_done(h, s);
+  }
+  if (!fusable && h->kind == 1 && !h->collective && !h->matc && h->r > 0 &&
+      !(h->graphs && !h->timing) && mlp_fused_enabled()) {
+    // n = 1 MLP round: gradient of every local learner and the fused update of
+    // the replicas and z in ONE cooperative kernel (sma_learner_mlp_fused.cu)
+    DeviceGuard guard(h->dev);
+    cudaStream_t s = (cudaStream_t)stream;
+    int buf = 0;
+    int64_t pos0 = 0;
+    STATUS_TRY(learner_batch(h, round, s, &buf, &pos0));
+    ReplicaArgs a{};
+    a.W = h->W;
+    a.ld = h->d_pad;
+    a.r = h->r;
+    a.d = h->cfg.d;
+    a.n4 = h->n4;
+    a.z = h->z();
+    a.zprev_next = h->zprev();
+    a.alpha = h->alpha;
+    a.gamma = h->gamma;
+    a.mu = h->mu;
+    a.nonfinite = h->check ? h->nonfinite : nullptr;
+    STATUS_TRY(pre_round(h, s, true));
+    cudaEvent_t* tp = nullptr;
+    STATUS_TRY(timer_pair(h, SMA_PHASE_REPLICA, &tp));
+    if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
+    const cudaError_t e = launch_mlp_round(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim,
+                                           h->hidden, h->classes, h->j0, h->mlp_PL, h->mlp_bar,
+                                           h->G, a, true, h->num_sms, s);
+    if (e != cudaErrorNotSupported) {
+      CUDA_TRY(e);
+      if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
+      h->launches += 1;
+      for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
+      leave_staged_set(h);
+      advance(h);
+      return mark_done(h, s);
+    }
+    if (tp) h->tused[SMA_PHASE_REPLICA] -= 2;  // nothing launched: drop the event pair
   }
   if (!fusable) {  // the same result through the two public calls
     STATUS_TRY(sma_learner_grads(h, round, stream));
@@ -1225,6 +1427,8 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
   }
   DeviceGuard guard(h->dev);
   cudaStream_t s = (cudaStream_t)stream;
+  leave_staged_set(h);
+  STATUS_TRY(pre_round(h, s, true));
   int buf = 0;
   int64_t pos0 = 0;
   STATUS_TRY(learner_batch(h, round, s, &buf, &pos0));

@@ -47,7 +47,8 @@ EXPORTS = ["sma_create", "sma_destroy", "sma_set_learner_grads", "sma_set_learne
            "sma_launch_count", "sma_info", "sma_last_error", "sma_abi_version",
            "sma_step_local", "sma_autotune_step", "sma_set_local_replicas", "sma_learner_step",
            "sma_p2p_handle", "sma_p2p_connect", "sma_set_alpha_global", "sma_get_reference",
-           "sma_set_reference", "sma_set_timing"]
+           "sma_set_reference", "sma_set_timing", "sma_stage_grads_host",
+           "sma_get_central_async", "sma_synchronize"]
 
 
 class SmaError(RuntimeError):
@@ -116,6 +117,9 @@ def load():
         "sma_get_reference": ([P, P, C.c_int], st),
         "sma_set_reference": ([P, P, C.c_int], st),
         "sma_set_timing": ([P, C.c_int], st),
+        "sma_stage_grads_host": ([P, i32, P], st),
+        "sma_get_central_async": ([P, P], st),
+        "sma_synchronize": ([P], st),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -167,6 +171,20 @@ def sma_set_learner_grads(h: int, j: int, g_dev) -> None:
 def sma_set_learner_grads_host(h: int, j: int, g_host, stream=None) -> None:
     _check(load().sma_set_learner_grads_host(h, j, _ptr(g_host), _stream(stream)),
            "sma_set_learner_grads_host")
+
+
+def sma_stage_grads_host(h: int, gset: int, g_hosts) -> None:
+    """g_hosts: one host buffer (pinned tensor / numpy array / address) per local learner."""
+    arr = (C.c_void_p * max(1, len(g_hosts)))(*[_ptr(g) for g in g_hosts])
+    _check(load().sma_stage_grads_host(h, gset, arr), "sma_stage_grads_host")
+
+
+def sma_get_central_async(h: int, z_host) -> None:
+    _check(load().sma_get_central_async(h, _ptr(z_host)), "sma_get_central_async")
+
+
+def sma_synchronize(h: int) -> None:
+    _check(load().sma_synchronize(h), "sma_synchronize")
 
 
 def sma_synth_grads(h: int, rnd: int, seed: int, stream=None) -> None:

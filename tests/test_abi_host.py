@@ -27,7 +27,7 @@ def test_exports_every_declared_symbol(lib):
     assert declared == set(sma.EXPORTS), declared ^ set(sma.EXPORTS)
     for name in declared:
         assert hasattr(lib, name), name
-    assert sma.sma_abi_version() == 1
+    assert sma.sma_abi_version() == 2
 
 
 def test_library_has_sm100a_code_and_no_torch_link():

@@ -369,6 +369,38 @@ def test_host_gradient_path_and_timing(torch_cuda, S, orc):
     h.close()
 
 
+@pytest.mark.parametrize("flags", [0, 16 | 1, 16 | 1 | 512])
+def test_pipelined_host_intake_and_async_readback(torch_cuda, S, orc, flags):
+    """The end-to-end path bench.py times (e2e): sma_stage_grads_host into the
+    two alternating gradient sets, sma_step, sma_get_central_async into a
+    distinct pinned buffer per round, one sma_synchronize at the end.  Every
+    round's read-back z equals the oracle's z after that round (the round two
+    steps later, which overwrites that z buffer, waited for the copy), and the
+    final state matches too."""
+    torch = torch_cuda
+    d, k, R = 100_003, 3, 12
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    h = S.Sma(d, k, a, g, m, sma_inputs.w0(d), flags=flags)
+    G = [[torch.from_numpy(sma_inputs.grad(i, j, k, d)).pin_memory() for j in range(k)]
+         for i in range(R)]
+    zouts = [torch.empty(d, dtype=torch.float32).pin_memory() for _ in range(R)]
+    s = torch.cuda.Stream()
+    for i in range(R):
+        S.sma_stage_grads_host(h.h, i & 1, G[i])
+        h.step(s)
+        S.sma_get_central_async(h.h, zouts[i])
+    S.sma_synchronize(h.h)
+    st = orc.State.init(sma_inputs.w0(d), k)
+    for i in range(R):
+        st.round(np.stack([G[i][j].numpy() for j in range(k)]), a, g, m)
+        assert relerr(zouts[i].numpy(), st.z) <= TOL, i
+    for j in range(k):
+        assert relerr(h.replica(j), st.W[j]) <= TOL
+    with pytest.raises(S.SmaError):
+        S.sma_stage_grads_host(h.h, 2, G[0])
+    h.close()
+
+
 # ------------------------------------------------- NEXT-3 / NEXT-4 on the GPU
 @pytest.mark.parametrize("flags", [0, 16, 16 | 1, 16 | 1 | 8])
 def test_sync_period_tau(torch_cuda, S, orc, flags):
@@ -549,27 +581,109 @@ def test_mlp_learner_sma_parity(torch_cuda, S, orc):
     h.close()
 
 
-@pytest.mark.parametrize("k", [4, 16, 12, 32])
-def test_mlp_bench_configs_100_rounds(torch_cuda, S, orc, k):
-    """The MLP bench configuration (`bench.py --config MLP --k K`): 784-256-10,
-    b = 16, alpha = 1/k, gamma = 0.1, mu = 0.9, w0 ~ N(0, 0.05) (seed 6),
-    60,000 MNIST-shaped blobs (seed 4), batch seed 99, sma_learner_step, 100
-    rounds vs the fp64 oracle at <= 1e-5 (north_star) on z, z_prev and every
-    replica.  The default learner policy puts layer 1 on the SIMT kernel at
-    k = 4 and 16 and on tcgen05 (3xTF32) at k = 12 and 32.
-    Precondition (R18), measured every round on every learner's batch: the
-    ReLU decisions at the GPU's fp32 state equal the oracle's."""
-    torch = torch_cuda
+MLP_BENCH = dict(b=16, seed=99, gamma=0.1, mu=0.9)   # bench.py --config MLP
+
+
+def mlp_bench_inputs(k):
+    """bench.py --config MLP --k K: 784-256-10, b = 16, alpha = 1/k, gamma = 0.1,
+    mu = 0.9, w0 ~ N(0, 0.05) (seed 6), 60,000 MNIST-shaped blobs (seed 4),
+    batch seed 99."""
     X, y = sma_inputs.blobs(60_000, seed=4)
-    b, R = 16, 100
-    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
     w0 = np.random.default_rng(6).normal(0, 0.05, MLP_D).astype(np.float32)
-    h, st, stats = mlp_sma_vs_oracle(torch, S, orc, X, y, k, b, 99, a, g, m, R, w0)
-    assert not stats["disagreements"], stats
-    assert relerr(h.central(), st.z) <= TOL, stats
-    assert relerr(h.central_prev(), st.z_prev) <= TOL, stats
-    for j in range(k):
-        assert relerr(h.replica(j), st.W[j]) <= TOL, (j, stats)
+    return X, y, w0, F32(1 / k), F32(MLP_BENCH["gamma"]), F32(MLP_BENCH["mu"])
+
+
+@pytest.mark.parametrize("k", [4, 16, 12, 32])
+def test_mlp_bench_configs_per_round_100_rounds(torch_cuda, S, orc, k):
+    """100 rounds of the MLP bench configuration (sma_learner_step: at n = 1 the
+    fused cooperative learner + update kernel) where EVERY round is checked
+    against the fp64 oracle run from the GPU's own state before that round (the
+    GPU's fp32 replicas, z and z_prev, promoted exactly): z, z_prev and every
+    replica after the round within 1e-6 (1 + |ref|), and each learner's
+    gradient, recovered in fp64 from the update (g = (w - c - w') / gamma,
+    c = alpha (w - z)), within 2e-6 of the oracle's.  Starting every round
+    from the same state makes the check independent of how an fp32 and an fp64
+    trajectory of this non-smooth learner drift apart (R18): the ReLU decisions
+    are taken on the same state by both sides."""
+    torch = torch_cuda
+    X, y, w0, a, g, m = mlp_bench_inputs(k)
+    b, seed = MLP_BENCH["b"], MLP_BENCH["seed"]
+    h = S.Sma(MLP_D, k, a, g, m, w0)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    S.sma_learner_attach(h.h, 1, 784, 256, 10, b, Xd, yd, X.shape[0], seed)
+    s = torch.cuda.Stream()
+    worst = dict(state=0.0, grad=0.0)
+    for i in range(100):
+        s.synchronize()
+        Wg = np.stack([h.replica(j) for j in range(k)]).astype(np.float64)
+        st = orc.State(Wg, h.central().astype(np.float64), h.central_prev().astype(np.float64))
+        G = np.stack([orc.mlp_loss_grad(X, y, orc.batch_indices(X.shape[0], k, b, seed, i, j),
+                                        Wg[j])[1] for j in range(k)])
+        z_before = st.z.copy()
+        st.round(G, a, g, m)
+        S.sma_learner_step(h.h, i, s)
+        s.synchronize()
+        zn = h.central()
+        worst["state"] = max(worst["state"], relerr(zn, st.z), relerr(h.central_prev(), st.z_prev))
+        for j in range(k):
+            wn = h.replica(j).astype(np.float64)
+            worst["state"] = max(worst["state"], relerr(wn, st.W[j]))
+            c = a * (Wg[j] - z_before)
+            gg = (Wg[j] - c - wn) / g
+            # 2e-6 (the single-gradient bar) + the fp32 rounding of w' and c, seen through / gamma
+            tol = 2e-6 + 2.0 ** -21 * (np.abs(Wg[j]) + np.abs(wn)) / g
+            worst["grad"] = max(worst["grad"], float(np.max(np.abs(gg - G[j]) / tol)))
+        assert worst["state"] <= 1e-6 and worst["grad"] <= 1.0, (i, worst)
+    print("MLP-PER-ROUND", dict(k=k, **worst))
+    h.close()
+
+
+@pytest.mark.parametrize("k", [4, 12, 16, 32])
+def test_mlp_bench_configs_trajectory_100_rounds(torch_cuda, S, orc, k):
+    """The same bench configuration run freely for 100 rounds on both sides (the
+    GPU's fp32 trajectory vs the oracle's fp64 one), at <= 1e-5 (north_star) on
+    z, z_prev and every replica after every round for as long as R18's
+    precondition holds: every ReLU decision at the GPU's state equals the
+    oracle's at its own state (measured per round on every learner's batch).
+    At k = 4 and 12 it holds for all 100 rounds (asserted).  At k = 16 and 32
+    the fp32-vs-fp64 state drift (~1e-6 in the pre-activations after tens of
+    rounds; R18) meets pre-activations within that distance of a kink (the
+    oracle's margin reaches ~3e-8 among 6.5M / 13M pre-activations), a decision
+    flips and the two trajectories legitimately separate; the test asserts
+    parity on every round before the first flip and records where it came."""
+    torch = torch_cuda
+    X, y, w0, a, g, m = mlp_bench_inputs(k)
+    b, seed = MLP_BENCH["b"], MLP_BENCH["seed"]
+    h = S.Sma(MLP_D, k, a, g, m, w0)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    S.sma_learner_attach(h.h, 1, 784, 256, 10, b, Xd, yd, X.shape[0], seed)
+    st = orc.State.init(w0.astype(np.float64), k)
+    s = torch.cuda.Stream()
+    drift, margin, first_flip, worst = 0.0, np.inf, None, 0.0
+    for i in range(100):
+        s.synchronize()
+        G = []
+        for j in range(k):
+            rows = orc.batch_indices(X.shape[0], k, b, seed, i, j)
+            ok, dr, mg = mlp_relu_decisions_agree(h.replica(j), st.W[j], X, rows)
+            drift, margin = max(drift, dr), min(margin, mg)
+            if not ok and first_flip is None:
+                first_flip = i
+            G.append(orc.mlp_loss_grad(X, y, rows, st.W[j])[1])
+        if first_flip is not None:
+            break
+        S.sma_learner_step(h.h, i, s)
+        st.round(np.stack(G), a, g, m)
+        s.synchronize()
+        e = max(relerr(h.central(), st.z), relerr(h.central_prev(), st.z_prev),
+                max(relerr(h.replica(j), st.W[j]) for j in range(k)))
+        worst = max(worst, e)
+        assert e <= TOL, (i, e)
+    print("MLP-TRAJECTORY", dict(k=k, rounds_in_parity=i if first_flip is not None else 100,
+                                 first_flip=first_flip, max_preact_drift=drift,
+                                 min_oracle_margin=margin, max_relerr=worst))
+    if k in (4, 12):
+        assert first_flip is None, (first_flip, drift, margin)
     h.close()
 
 
@@ -768,12 +882,12 @@ def test_learner_step_overlapped_zsync(torch_cuda, S, orc, kind, variant):
 @pytest.mark.parametrize("k,b", [(3, 16), (9, 16), (4, 5)])
 def test_mlp_layer1_tensor_cores_vs_simt_and_oracle(torch_cuda, orc, tmp_path, k, b):
     """NEXT-2: the MLP's layer-1 GEMM on tcgen05 (3xTF32 + |.|-bound MMAs, K split
-    over a 7-CTA cluster; SMA_MLP_TC=1) and the SIMT kernel (SMA_MLP_TC=0) give
-    the same gradients to ~1e-7 -- so do the mixed policies (layer 1 only:
-    "hidden", the default from r >= 12; dW1 only: "w1") -- and all match the
-    fp64 oracle < 2e-6 (ragged
-    batch b = 5 pads N = 16 with zero rows); the ReLU mask is decided at
-    fp64-level accuracy on both paths (R18)."""
+    over a 7-CTA cluster; SMA_MLP_TC=1), the five-kernel SIMT path (SMA_MLP_TC=0),
+    the mixed policies (layer 1 only: "hidden"; dW1 only: "w1") and the default
+    fused cooperative kernel (SMA_MLP_TC unset: sma_learner_mlp_fused.cu) give
+    the same gradients to ~1e-7 and all match the fp64 oracle < 2e-6 (ragged
+    batch b = 5 pads the 16 rows with zeros); the ReLU mask is decided at
+    fp64-level accuracy on every path (R18)."""
     import os
     import subprocess
     import sys
@@ -781,10 +895,13 @@ def test_mlp_layer1_tensor_cores_vs_simt_and_oracle(torch_cuda, orc, tmp_path, k
     X, y = sma_inputs.blobs(2_000, seed=12)
     rnd, seed = 7, 31
     got = {}
-    modes = ("0", "1", "hidden", "w1")
+    modes = ("0", "fused", "1", "hidden", "w1")   # "fused": SMA_MLP_TC unset, the default kernel
     for tc in modes:
         out = str(tmp_path / f"g{tc}.npy")
         env = dict(os.environ, SMA_MLP_TC=tc)
+        if tc == "fused":
+            env.pop("SMA_MLP_TC")
+            env.pop("SMA_MLP_FUSED", None)
         subprocess.check_call([sys.executable, worker, out, str(k), str(b), str(rnd), str(seed)],
                               env=env, timeout=300)
         got[tc] = np.load(out)
