@@ -259,6 +259,80 @@ def arm_config(args, world, d, d_pad, k, alpha, gamma, mu, zsync=None, push=Fals
                   f"{(alg_bytes / 1e9):.2f} GB/GPU >> 126 MB L2"}
 
 
+def nvlink_counters(device):
+    """Cumulative NVLink data counters of one GPU (KiB transmitted / received,
+    summed over its links) from `nvidia-smi nvlink -gt d`; None where the GPU
+    has no NVLink or the query is unsupported."""
+    try:
+        out = subprocess.run(["nvidia-smi", "nvlink", "-gt", "d", "-i", str(device)],
+                             capture_output=True, text=True, timeout=10).stdout
+    except Exception:  # noqa: BLE001
+        return None
+    tx = rx = 0
+    seen = False
+    for line in out.splitlines():
+        low = line.lower()
+        if "kib" not in low:
+            continue
+        try:
+            val = int(line.split(":")[-1].strip().split()[0])
+        except (ValueError, IndexError):
+            continue
+        if "tx" in low:
+            tx += val
+            seen = True
+        elif "rx" in low:
+            rx += val
+            seen = True
+    return (tx * 1024, rx * 1024) if seen else None
+
+
+def nvlink_block(zsync, mode, world, d_pad, phase_avg, serial, link_counters, rank_info):
+    """NVLink side of the metric for the collective path.  Link bytes are
+    counted PER DIRECTION per GPU and compared with the 770 GB/s per-direction
+    peer bandwidth, so frac <= 1 holds by construction:
+      NCCL ring RS, AG:        4 d_pad (n-1)/n each (nccl-tests busBW convention),
+                               run one after the other;
+      fused P2P z-sync (pull): ingress = the n-1 peers' partial shards and egress =
+                               this GPU's z shard to n-1 peers, 4 d_pad (n-1)/n each way,
+                               concurrently in one kernel (push: the same bytes, the
+                               partial leg during the replica kernel);
+      NVLS z-sync:             ~4 d_pad per direction (multimem ld_reduce / st)."""
+    one = 4 * d_pad * (world - 1) / world
+    rs_ms, up_ms, ag_ms, fz_ms = phase_avg[1], phase_avg[2], phase_avg[3], phase_avg[4]
+    gbs = lambda b, ms_: (b / (ms_ * 1e-3) / 1e9) if ms_ > 0 else None  # noqa: E731
+    per_dir = one if zsync in ("p2p", "nccl") else 4 * d_pad
+    if fz_ms > 0:
+        bus = gbs(per_dir, fz_ms)
+        how = "fused z-sync kernel: per-direction link bytes / its event time"
+    else:
+        bus = gbs(2 * one, rs_ms + ag_ms)   # RS then AG, each 4 d_pad (n-1)/n per direction
+        how = "NCCL RS + AG (sequential): per-direction link bytes of both / their summed time"
+    blk = {
+        "zsync": zsync, "link_bytes_per_direction_per_gpu_per_round": per_dir if fz_ms > 0
+        else 2 * one,
+        "reduce_scatter_ms": rs_ms, "shard_update_ms": up_ms, "all_gather_ms": ag_ms,
+        "fused_zsync_ms": fz_ms, "rs_bus_gbs": gbs(one, rs_ms), "ag_bus_gbs": gbs(one, ag_ms),
+        "bus_gbs_per_direction": bus, "peak_gbs_per_direction": NVLINK_PEAK_GBS,
+        "frac": (bus / NVLINK_PEAK_GBS) if bus else None, "how": how,
+        "note": "times from CUDA events around each phase on its stream, max over ranks" +
+                ("; in Mode B the z-sync runs concurrently with the replica kernel"
+                 if mode == "B" else ""),
+        "ranks": rank_info}
+    if serial is not None:
+        s_rs, s_ag, s_fz = serial[2], serial[4], serial[5]
+        s_bus = gbs(per_dir, s_fz) if s_fz > 0 else gbs(2 * one, s_rs + s_ag)
+        blk["serial_mode_a"] = {
+            "ms_per_round": serial[0], "replica_ms": serial[1], "reduce_scatter_ms": s_rs,
+            "shard_update_ms": serial[3], "all_gather_ms": s_ag, "fused_zsync_ms": s_fz,
+            "bus_gbs_per_direction": s_bus,
+            "frac": (s_bus / NVLINK_PEAK_GBS) if s_bus else None,
+            "note": "separate Mode-A handle, same workload, z-sync not overlapped"}
+    if link_counters is not None:
+        blk["measured_link_bytes"] = link_counters
+    return blk
+
+
 def workload_name(cfg, d, k):
     names = {"C2": "LeNet-sized", "C3": "ResNet-32-sized", "C4": "ResNet-50-sized",
              "C5": "VGG-16-sized", "C1": "softmax-regression learner in the loop,",
@@ -372,6 +446,20 @@ def main():
     else:
         h = make_handle(flags)
     r = h.local_count
+    rank_info = None
+    if collective:   # per-rank evidence: device identity and the peer mapping that ran
+        pr = torch.cuda.get_device_properties(local)
+        me = {"rank": rank, "local_rank": local, "device": pr.name,
+              "uuid": str(getattr(pr, "uuid", "")),
+              "pci_bus_id": getattr(pr, "pci_bus_id", None),
+              "zsync": zsync, "p2p_peers_mapped": (world - 1) if zsync == "p2p" else 0,
+              "can_access_peer": [bool(torch.cuda.can_device_access_peer(local, q))
+                                  for q in range(torch.cuda.device_count()) if q != local]}
+        rank_info = [None] * world
+        if world > 1:
+            dist.all_gather_object(rank_info, me)
+        else:
+            rank_info = [me]
     stream = torch.cuda.Stream()
     rnd = [0]
     if learner:   # MNIST-shaped synthetic blobs resident in HBM, learner in the loop
@@ -467,6 +555,7 @@ def main():
     # workload) runs a short serial pass: its reduce-scatter / all-gather times
     # give the uncontended NVLink bus bandwidth (nccl-tests convention).
     serial = None
+    link_counters = None
     if collective and mode == "B" and zsync in ("nccl", "p2p"):
         nccl_id_main, nccl_id = nccl_id, nccl_id_a   # the second handle's own communicator
         hA = make_handle((flags & ~sma.FLAG_OVERLAP) | sma.FLAG_TIMING)
@@ -479,11 +568,27 @@ def main():
             hA.kernel_time(reset=True, phase=ph)
         ns = max(10, args.steps // 4)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0 = nvlink_counters(local)
         e0.record(stream)
         for _ in range(ns):
             hA.step(stream)
         e1.record(stream)
         barrier()
+        c1 = nvlink_counters(local)
+        mine = None
+        if c0 is not None and c1 is not None:
+            mine = {"rank": rank, "tx_bytes_per_round": (c1[0] - c0[0]) / ns,
+                    "rx_bytes_per_round": (c1[1] - c0[1]) / ns}
+        allc = [None] * world
+        if world > 1:
+            dist.all_gather_object(allc, mine)   # every rank joins, counters or not
+        else:
+            allc = [mine]
+        if any(x is not None for x in allc):
+            link_counters = {"serial_mode_a_pass": allc,
+                             "source": "nvidia-smi nvlink -gt d (cumulative data KiB over all "
+                                       "links of each rank's GPU), delta over the serial "
+                                       "Mode-A pass / its rounds"}
         pa = []
         for ph in range(5):
             pm, pn = hA.kernel_time(reset=True, phase=ph)
@@ -598,36 +703,8 @@ def main():
             "clocks": clk,
         }
         if collective:
-            one = 4 * d_pad * (world - 1) / world      # bus bytes of one RS (or AG) per GPU
-            rs_ms, up_ms, ag_ms, nv_ms = phase_avg[1], phase_avg[2], phase_avg[3], phase_avg[4]
-            bus = lambda ms_: (one / (ms_ * 1e-3) / 1e9) if ms_ > 0 else None  # noqa: E731
-            comb = (2 * one / ((rs_ms + ag_ms) * 1e-3) / 1e9) if rs_ms + ag_ms > 0 else None
-            if nv_ms > 0:   # fused z-sync kernel: same bus-byte convention over its time
-                comb = 2 * one / (nv_ms * 1e-3) / 1e9
-            line["nvlink"] = {
-                "bus_bytes_per_gpu_per_round": 2 * one,
-                "zsync": zsync,
-                "reduce_scatter_ms": rs_ms, "shard_update_ms": up_ms, "all_gather_ms": ag_ms,
-                "fused_zsync_ms": nv_ms,
-                "rs_bus_gbs": bus(rs_ms), "ag_bus_gbs": bus(ag_ms), "bus_gbs": comb,
-                "peak_gbs": NVLINK_PEAK_GBS,
-                "frac": (comb / NVLINK_PEAK_GBS) if comb else None,
-                "note": "nccl-tests bus convention busBW = 4 d_pad (n-1)/n / t per collective; "
-                        "times from CUDA events around each NCCL call on its stream, max over "
-                        "ranks" + ("; in Mode B they run concurrently with the replica kernel"
-                                   if mode == "B" else "")}
-            if serial is not None:
-                s_rs, s_ag, s_fz = serial[2], serial[4], serial[5]
-                s_comb = (2 * one / ((s_rs + s_ag) * 1e-3) / 1e9) if s_rs + s_ag > 0 else None
-                if s_fz > 0:
-                    s_comb = 2 * one / (s_fz * 1e-3) / 1e9
-                line["nvlink"]["serial_mode_a"] = {
-                    "ms_per_round": serial[0], "replica_ms": serial[1],
-                    "reduce_scatter_ms": s_rs, "shard_update_ms": serial[3],
-                    "all_gather_ms": s_ag, "fused_zsync_ms": s_fz,
-                    "rs_bus_gbs": bus(s_rs), "ag_bus_gbs": bus(s_ag),
-                    "bus_gbs": s_comb, "frac": (s_comb / NVLINK_PEAK_GBS) if s_comb else None,
-                    "note": "separate Mode-A handle, same workload, z-sync not overlapped"}
+            line["nvlink"] = nvlink_block(zsync, mode, world, d_pad, phase_avg, serial,
+                                          link_counters, rank_info)
         if shared:
             line["config"]["shared_gpu_test"] = ("all ranks time-share cuda:0 "
                                                  "(SMA_BENCH_SHARED_GPU): a code-path test, not a "

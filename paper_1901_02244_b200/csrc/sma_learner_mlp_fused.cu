@@ -39,6 +39,7 @@
 // return cudaErrorNotSupported and the caller uses the five-kernel path.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include "sma_bulk.cuh"
@@ -121,8 +122,17 @@ struct MlpRoundArgs {
   float* PL;              // [r][nblk][kRows][classes] partial logits
   float* G;               // gradients [r][ld]
   unsigned* bar;          // grid barrier state [2]
+  unsigned long long* prof;  // SMA_MLP_PROF: globaltimer stamps of CTA 0 (or nullptr)
   ReplicaArgs a;          // W, ld, r, z, zprev_next, alpha, gamma, mu, d, n4, nonfinite
 };
+
+__device__ __forceinline__ void stamp(const MlpRoundArgs& m, int i) {
+  if (m.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    m.prof[i] = t;
+  }
+}
 
 // sma_elem / central_elem of sma_kernels.cu.
 __device__ __forceinline__ float elem_w(float w, float g, float z, float alpha, float gamma,
@@ -145,7 +155,8 @@ __global__ void __launch_bounds__(kThr, 1) mlp_round_kernel(const MlpRoundArgs m
   float* es = lg + kRows * 32;                      // [kRows][32] softmax - onehot
   float* xn = es + kRows * 32;                      // [kRows] ||x_t||
   float* wn = xn + kRows;                           // [U] ||W1[u]||
-  unsigned char* msk = reinterpret_cast<unsigned char*>(wn + U);  // [kRows][U]
+  float* w2s = wn + U;                              // [32][U] W2 columns of my units
+  unsigned char* msk = reinterpret_cast<unsigned char*>(w2s + 32 * U);  // [kRows][U]
   __shared__ int rows[kRows], ys[kRows];
   __shared__ int n_unc;
   __shared__ short unc[kRows * 64];
@@ -162,6 +173,7 @@ __global__ void __launch_bounds__(kThr, 1) mlp_round_kernel(const MlpRoundArgs m
   float* G = m.G + (int64_t)j * m.a.ld;
 
   // ---- prologue (X, perm, y are never written by a kernel: before the PDL wait)
+  stamp(m, 0);
   if (tid < kRows) {
     const int r = tid < b ? m.perm[m.pos0 + (int64_t)(m.j0 + j) * b + tid] : 0;
     rows[tid] = r;
@@ -184,7 +196,9 @@ __global__ void __launch_bounds__(kThr, 1) mlp_round_kernel(const MlpRoundArgs m
     for (int off = 16; off >= 1; off >>= 1) s = __fadd_rn(s, __shfl_xor_sync(0xffffffffu, s, off));
     if (lane == 0) xn[t] = sqrtf(s);
   }
+  stamp(m, 1);
   pdl::wait_and_release();  // the replicas (W) were written by the previous round
+  stamp(m, 2);
 
   // ---- phase 1: a1 = W1 x + b1 for (16 rows x U units), K split over the warps
   {
@@ -201,6 +215,7 @@ __global__ void __launch_bounds__(kThr, 1) mlp_round_kernel(const MlpRoundArgs m
     }
     const float4* xr0 = reinterpret_cast<const float4*>(xs + t0 * in_dim);
     const float4* xr1 = reinterpret_cast<const float4*>(xs + (t0 + 1) * in_dim);
+#pragma unroll 2
     for (int k4 = k4a; k4 < k4b; ++k4) {
       float4 wv[TU];
 #pragma unroll
@@ -281,23 +296,39 @@ __global__ void __launch_bounds__(kThr, 1) mlp_round_kernel(const MlpRoundArgs m
     }
   }
   __syncthreads();
-  // partial logits of this unit block
+  stamp(m, 3);
+  // partial logits of this unit block (W2's columns of the block staged once)
+  for (int q = tid; q < classes * U; q += kThr) {
+    const int c = q / U, ul = q - c * U;
+    w2s[q] = ld_w(W2 + (int64_t)c * hidden + u0 + ul);
+  }
+  __syncthreads();
   float* PL = m.PL + (int64_t)blockIdx.x * kRows * classes;
   for (int q = tid; q < kRows * classes; q += kThr) {
     const int t = q / classes, c = q - t * classes;
-    const float* w2 = W2 + (int64_t)c * hidden + u0;
     float s = 0.f;
-    for (int ul = 0; ul < U; ++ul) s = __fmaf_rn(ld_w(w2 + ul), hs[t * U + ul], s);
+#pragma unroll 8
+    for (int ul = 0; ul < U; ++ul) s = __fmaf_rn(w2s[c * U + ul], hs[t * U + ul], s);
     PL[q] = s;
   }
+  stamp(m, 4);
   grid_barrier(m.bar);
+  stamp(m, 5);
 
   // ---- phase 2: logits, softmax, head, dW1 for this unit block
   const float* PLj = m.PL + (int64_t)j * m.nblk * kRows * classes;
   for (int q = tid; q < b * classes; q += kThr) {
     const int t = q / classes, c = q - t * classes;
     float s = 0.f;
-    for (int k = 0; k < m.nblk; ++k) s = __fadd_rn(s, ld_cg(PLj + (int64_t)k * kRows * classes + q));
+    int k = 0;
+    for (; k + 8 <= m.nblk; k += 8) {  // 8 loads in flight, added in ascending blk
+      float v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = ld_cg(PLj + (int64_t)(k + i) * kRows * classes + q);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s = __fadd_rn(s, v[i]);
+    }
+    for (; k < m.nblk; ++k) s = __fadd_rn(s, ld_cg(PLj + (int64_t)k * kRows * classes + q));
     lg[t * 32 + c] = __fadd_rn(s, ld_w(b2 + c));
   }
   __syncthreads();
@@ -322,8 +353,7 @@ __global__ void __launch_bounds__(kThr, 1) mlp_round_kernel(const MlpRoundArgs m
     const int t = q / U, ul = q - t * U;
     float s = 0.f;
     if (t < b)
-      for (int c = 0; c < classes; ++c)
-        s = __fmaf_rn(ld_w(W2 + (int64_t)c * hidden + u0 + ul), es[t * 32 + c], s);
+      for (int c = 0; c < classes; ++c) s = __fmaf_rn(w2s[c * U + ul], es[t * 32 + c], s);
     das[q] = msk[q] ? s : 0.f;
   }
   __syncthreads();
@@ -355,8 +385,10 @@ __global__ void __launch_bounds__(kThr, 1) mlp_round_kernel(const MlpRoundArgs m
       reinterpret_cast<float4*>(G + (int64_t)(u0 + ul) * in_dim)[f4] = s;
     }
   }
+  stamp(m, 6);
   if (!UPDATE) return;
   grid_barrier(m.bar);
+  stamp(m, 7);
 
   // ---- phase 3: the fused n = 1 round over all parameters (a3-a7)
   const ReplicaArgs& a = m.a;
@@ -405,11 +437,12 @@ __global__ void __launch_bounds__(kThr, 1) mlp_round_kernel(const MlpRoundArgs m
     bad |= !(isfinite(zn.x) && isfinite(zn.y) && isfinite(zn.z) && isfinite(zn.w));
   }
   if (a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
+  stamp(m, 8);
 }
 
 size_t round_smem(int in_dim, int U) {
   return sizeof(float) * ((size_t)kRows * in_dim + (size_t)kWarps * kRows * U + (size_t)kWarps * U +
-                          2 * (size_t)kRows * U + 2 * (size_t)kRows * 32 + kRows + U) +
+                          2 * (size_t)kRows * U + 2 * (size_t)kRows * 32 + kRows + U + 32 * (size_t)U) +
          (size_t)kRows * U + 16;
 }
 
@@ -438,6 +471,23 @@ cudaError_t launch_tu(const MlpRoundArgs& m, int grid, size_t smem, cudaStream_t
   return cudaLaunchKernelEx(&cfg, k, m);
 }
 }  // namespace
+
+// SMA_MLP_PROF=N (debugging only): CTA 0 stamps %globaltimer at the phase
+// boundaries of every launch and the launcher prints launch N's phase times
+// (us) to stderr, synchronising the stream after that launch.
+static int prof_launch() {
+  static const int n = [] {
+    const char* e = getenv("SMA_MLP_PROF");
+    return e ? atoi(e) : 0;
+  }();
+  return n;
+}
+unsigned long long* mlp_prof_buffer() {
+  static unsigned long long* buf = nullptr;
+  if (prof_launch() > 0 && !buf && cudaMalloc(&buf, 16 * sizeof(unsigned long long)) != cudaSuccess)
+    buf = nullptr;
+  return buf;
+}
 
 bool mlp_fused_enabled() {
   static const bool on = [] {
@@ -470,9 +520,12 @@ cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* pe
   m.b = b; m.in_dim = in_dim; m.hidden = hidden; m.classes = classes; m.j0 = j0;
   m.U = U; m.nblk = hidden / U;
   m.PL = PL; m.G = G; m.bar = bar; m.a = a;
+  m.prof = mlp_prof_buffer();
   const int grid = a.r * m.nblk;
-#define SMA_MLP_ROUND(TU)                                                              \
-  return update ? launch_tu<TU, true>(m, grid, smem, s) : launch_tu<TU, false>(m, grid, smem, s);
+  cudaError_t e;
+#define SMA_MLP_ROUND(TU)                                                                      \
+  e = update ? launch_tu<TU, true>(m, grid, smem, s) : launch_tu<TU, false>(m, grid, smem, s); \
+  break;
   switch (U / kUG) {
     case 1: SMA_MLP_ROUND(1)
     case 2: SMA_MLP_ROUND(2)
@@ -481,6 +534,18 @@ cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* pe
     default: SMA_MLP_ROUND(16)
   }
 #undef SMA_MLP_ROUND
+  static int launches = 0;
+  if (m.prof && e == cudaSuccess && ++launches == prof_launch()) {
+    unsigned long long t[16] = {};
+    cudaStreamSynchronize(s);
+    cudaMemcpy(t, m.prof, sizeof t, cudaMemcpyDeviceToHost);
+    const char* names[] = {"prologue", "pdl_wait", "phase1", "partial_logits", "barrier1",
+                           "phase2", "barrier2", "phase3"};
+    fprintf(stderr, "SMA_MLP_PROF launch %d (r=%d U=%d grid=%d):", launches, a.r, U, grid);
+    for (int i = 0; i < 8; ++i) fprintf(stderr, " %s=%.2f", names[i], (t[i + 1] - t[i]) * 1e-3);
+    fprintf(stderr, " total=%.2f us\n", (t[8] - t[0]) * 1e-3);
+  }
+  return e;
 }
 
 }  // namespace sma

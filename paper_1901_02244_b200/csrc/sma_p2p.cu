@@ -43,6 +43,14 @@ __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -183,14 +191,25 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
   if (a.nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(a.nonfinite, 1);
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence_system();  // my peer stores before my arrival
-    const unsigned prev = atomicAdd(a.ctl + 2, 1u);
+    // Barrier B.  Each CTA's arrival is a gpu-scope release (it orders the CTA's
+    // peer stores, made visible to thread 0 by the bar.sync above) and the last
+    // arrival's acquire sees them all; its system-scope release to every peer is
+    // cumulative, so a peer that acquires the flag sees every store of this
+    // rank's grid (PTX causality order is transitive across the two scopes).
+    // Round 1 ran a __threadfence_system per CTA instead: 53 % of the stall
+    // samples of the C3 z-sync (profiles/r02_ncu_p2p_c3.txt).
+    const unsigned prev = BAR ? atom_add_acq_rel_gpu(a.ctl + 2, 1u)
+                              : (__threadfence_system(), atomicAdd(a.ctl + 2, 1u));
     if (prev == gridDim.x - 1) {  // the last CTA of this rank closes the round
-      __threadfence_system();
+      if (!BAR) __threadfence_system();
       a.ctl[2] = 0;
       const unsigned tB = a.ctl[1] + 1u;
-      for (int g = 0; g < n; ++g)  // barrier B: my shard has landed everywhere
-        st_release_sys(reinterpret_cast<unsigned*>(a.base[g] + a.off_flags) + 64 + a.rank, tB);
+      if (BAR) asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int g = 0; g < n; ++g) {  // barrier B: my shard has landed everywhere
+        unsigned* f = reinterpret_cast<unsigned*>(a.base[g] + a.off_flags) + 64 + a.rank;
+        if (BAR) st_relaxed_sys(f, tB);   // fence.release + strong write = release pattern
+        else st_release_sys(f, tB);
+      }
       wait_all(reinterpret_cast<const unsigned*>(a.base[a.rank] + a.off_flags) + 64, n, tB);
       a.ctl[0] = s_targetA;
       a.ctl[1] = tB;
@@ -201,10 +220,11 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
 }  // namespace
 
 cudaError_t launch_zsync_p2p(int mode, const P2PArgs& a, int num_ctas, cudaStream_t s) {
-  // A persistent grid (num_ctas: #SMs x 4): every CTA pays one system-scope
-  // acquire (barrier A) and one system fence + arrival (barrier B), so a full
-  // grid of ~25k CTAs spent more time in those than in moving data.
-  const int64_t want = (a.len4 + kP2PThreads - 1) / kP2PThreads;
+  // A persistent grid (at most num_ctas: #SMs x 4) sized so every thread has
+  // >= 4 float4 chunks of the shard (2 per loop iteration): the per-CTA barrier
+  // work (one device-scope wait, one arrival) is then amortised, and a small
+  // shard (C3 at n = 8: 14.5k chunks) runs on a few CTAs instead of ~450.
+  const int64_t want = (a.len4 + 4 * kP2PThreads - 1) / (4 * kP2PThreads);
   int grid = (int)((num_ctas > 0 && want > num_ctas) ? num_ctas : want);
   if (grid < 1) grid = 1;
   // Launched without PDL (no measurable gain on one GPU: C3 Mode A 41-46k rounds/s

@@ -450,7 +450,13 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
       const int v = e ? atoi(e) : 4;
       return v >= 1 && v <= 8 ? v : 4;
     }();
-    CUDA_TRY(launch_zsync_p2p(mode, a, per_sm * h->num_sms, s));  // Mode B: high-priority stream
+    // SMA_P2P_CTAS (experiments): an absolute cap on the grid, e.g. the few SMs
+    // that saturate NVLink while the concurrent replica kernel keeps the rest
+    static const int cap = [] {
+      const char* e = getenv("SMA_P2P_CTAS");
+      return e ? atoi(e) : 0;
+    }();
+    CUDA_TRY(launch_zsync_p2p(mode, a, cap > 0 ? cap : per_sm * h->num_sms, s));  // Mode B: high-priority stream
     if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
     return SMA_OK;
   }
