@@ -31,6 +31,15 @@ __device__ __forceinline__ f2 f2_add(f2 a, f2 b) {
   r.lo = __fadd_rn(__fadd_rn(a.lo, b.lo), e);
   return r;
 }
+// The ReLU decision [a > 0] on a double-float a = hi + lo.  hi is NOT the
+// rounded value of the pair: neither dot2_step nor f2_add renormalises, so after
+// cancellation |lo| can exceed |hi| (lo collects every rounding error of the
+// running sum) and sign(hi) can differ from sign(hi + lo).  fl(hi + lo) has the
+// sign of hi + lo exactly (round-to-nearest keeps the sign and returns 0 only
+// for an exact 0), so the decision is taken on it.  (Deciding on hi first
+// flipped a mask at a1 = +1.3e-8 in the k = 32 MLP parity test.)
+__device__ __forceinline__ bool positive(float hi, float lo) { return __fadd_rn(hi, lo) > 0.f; }
+
 // Warp-wide sum of per-lane double-float partials (every lane gets the total).
 __device__ __forceinline__ f2 warp_sum(f2 acc) {
 #pragma unroll

@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_logits_kernel(
   pdl::wait_and_release();
   for (int k = threadIdx.x; k < hidden; k += blockDim.x) {  // relu of the double-float a1
     const float2 v = a1[k];
-    hrow[k] = (v.x > 0.f || (v.x == 0.f && v.y > 0.f)) ? __fadd_rn(v.x, v.y) : 0.f;
+    hrow[k] = dot2::positive(v.x, v.y) ? __fadd_rn(v.x, v.y) : 0.f;
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_head_kernel(
                         1, 2 * b * hidden, 0, 0, w2s, W2, classes * hidden, &bar, 0, true);
   for (int q = threadIdx.x; q < b * hidden; q += blockDim.x) {
     const float2 v = a1[q];
-    hs[q] = (v.x > 0.f || (v.x == 0.f && v.y > 0.f)) ? __fadd_rn(v.x, v.y) : 0.f;
+    hs[q] = dot2::positive(v.x, v.y) ? __fadd_rn(v.x, v.y) : 0.f;
   }
   __syncthreads();
   const float fb = (float)b;
@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_head_kernel(
     float s = 0.f;
     for (int c = 0; c < classes; ++c) s = __fmaf_rn(w2s[c * hidden + k], e[t * classes + c], s);
     const float2 v = a1[q];
-    DA[(int64_t)slot * b * hidden + q] = (v.x > 0.f || (v.x == 0.f && v.y > 0.f)) ? s : 0.f;
+    DA[(int64_t)slot * b * hidden + q] = dot2::positive(v.x, v.y) ? s : 0.f;
   }
 }
 

@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kThr, 1) mlp_round_kernel(const MlpRoundArgs m
     }
     acc = dot2::f2_add(dot2::warp_sum(acc), f2{ld_w(b1 + u0 + ul), 0.f});
     if (lane == 0) {
-      const bool on = acc.hi > 0.f || (acc.hi == 0.f && acc.lo > 0.f);
+      const bool on = dot2::positive(acc.hi, acc.lo);
       hs[q] = on ? __fadd_rn(acc.hi, acc.lo) : 0.f;
       msk[q] = on ? 1 : 0;
     }
