@@ -125,8 +125,8 @@ int mlp_tc_policy();
 bool mlp_fused_enabled();
 cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* perm, int64_t pos0,
                              int b, int in_dim, int hidden, int classes, int j0, float* PL,
-                             unsigned* bar, float* G, const ReplicaArgs& a, bool update,
-                             int num_sms, cudaStream_t s);
+                             unsigned* bar, unsigned epoch, float* G, const ReplicaArgs& a,
+                             bool update, int num_sms, cudaStream_t s);
 // MLP layer 1 on tcgen05 (3xTF32 + |.| bound MMAs, cluster K-split); returns
 // cudaErrorNotSupported without launching when the shape is outside its path.
 cudaError_t launch_mlp_hidden_tc(const float* X, const int32_t* perm, int64_t pos0, int b,

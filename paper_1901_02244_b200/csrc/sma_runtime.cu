@@ -140,7 +140,8 @@ struct sma_handle {
   float* mlp_DA = nullptr;
   float* mlp_E = nullptr;
   float* mlp_PL = nullptr;     // fused MLP round: partial logits [num_sms][16][32]
-  unsigned* mlp_bar = nullptr; // fused MLP round: grid barrier state [2]
+  unsigned* mlp_bar = nullptr; // fused MLP round: flag lines [2 num_sms][32]
+  unsigned mlp_epoch = 0;      // fused MLP round: launches so far (the flags' epoch)
   const float* X = nullptr;
   const int32_t* y = nullptr;
   int64_t n_samples = 0;
@@ -1255,9 +1256,10 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
       h->mlp_E = nullptr;
       CUDA_TRY(cudaMalloc(&h->mlp_E, sizeof(float) * (size_t)SMA_MAX_LOCAL_REPLICAS * batch * classes));
       if (!h->mlp_PL) CUDA_TRY(cudaMalloc(&h->mlp_PL, sizeof(float) * (size_t)h->num_sms * 16 * 32));
-      if (!h->mlp_bar) {
-        CUDA_TRY(cudaMalloc(&h->mlp_bar, 2 * sizeof(unsigned)));
-        CUDA_TRY(cudaMemset(h->mlp_bar, 0, 2 * sizeof(unsigned)));
+      if (!h->mlp_bar) {  // two kinds of 128-byte flag lines, one per CTA (grid <= #SMs)
+        const size_t nb = sizeof(unsigned) * 32 * 2 * (size_t)h->num_sms;
+        CUDA_TRY(cudaMalloc(&h->mlp_bar, nb));
+        CUDA_TRY(cudaMemset(h->mlp_bar, 0, nb));
       }
     }
     CUDA_TRY(cudaMalloc(&h->mlp_DA, sizeof(float) * n));
@@ -1340,7 +1342,7 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
     a.ld = h->d_pad;
     a.r = h->r;
     cudaError_t e = launch_mlp_round(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim,
-                                     h->hidden, h->classes, h->j0, h->mlp_PL, h->mlp_bar, h->G, a,
+                                     h->hidden, h->classes, h->j0, h->mlp_PL, h->mlp_bar, ++h->mlp_epoch, h->G, a,
                                      false, h->num_sms, s);
     if (e == cudaErrorNotSupported) {  // the five-kernel path
       CUDA_TRY(launch_mlp_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim, h->hidden,
@@ -1415,7 +1417,7 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
     if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
     const cudaError_t e = launch_mlp_round(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim,
                                            h->hidden, h->classes, h->j0, h->mlp_PL, h->mlp_bar,
-                                           h->G, a, true, h->num_sms, s);
+                                           ++h->mlp_epoch, h->G, a, true, h->num_sms, s);
     if (e != cudaErrorNotSupported) {
       CUDA_TRY(e);
       if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
