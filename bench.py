@@ -70,6 +70,10 @@ def parse():
     ap.add_argument("--hier", action="store_true",
                     help="Section 3.3 two-level rule (per-GPU reference models, R20): "
                          "alpha_l = 1/(2r), alpha_g = 1/(2(N-1)); identical to flat SMA at N = 1")
+    ap.add_argument("--rounds-per-call", type=int, default=1,
+                    help="learner configs: rounds per sma_learner_steps call (the MLP learner "
+                         "then runs the rounds of one epoch in one launch of its fused kernel); "
+                         "1 = one sma_learner_step per round")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -469,20 +473,29 @@ def main():
                                256 if args.config == "MLP" else 0, 10, cfg["batch"], Xd, yd,
                                X.shape[0], 99)
 
-        def one_step():   # learner gradient + round (fused for the softmax learner)
-            sma.sma_learner_step(h.h, rnd[0], stream)
-            rnd[0] += 1
+        def run_steps(n):   # learner gradient + round, n rounds
+            if args.rounds_per_call <= 1:
+                for _ in range(n):
+                    sma.sma_learner_step(h.h, rnd[0], stream)
+                    rnd[0] += 1
+                return
+            while n > 0:
+                c = min(n, args.rounds_per_call)
+                sma.sma_learner_steps(h.h, rnd[0], c, stream)
+                rnd[0] += c
+                n -= c
     else:
         h.synth_grads(0, sma_inputs.SEED_G, stream)   # inputs resident in HBM before timing
 
-        def one_step():
+        def run_steps(n):
             # tau = 1: every iteration is a full SMA round; tau > 1 / 0: the E11
             # analog with local-only iterations in between
-            rnd[0] += 1
-            if args.tau == 1 or (args.tau > 1 and rnd[0] % args.tau == 0):
-                h.step(stream)
-            else:
-                h.step_local(stream)
+            for _ in range(n):
+                rnd[0] += 1
+                if args.tau == 1 or (args.tau > 1 and rnd[0] % args.tau == 0):
+                    h.step(stream)
+                else:
+                    h.step_local(stream)
     stream.synchronize()
 
     def barrier():
@@ -499,8 +512,7 @@ def main():
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
-    for _ in range(args.warmup):
-        one_step()
+    run_steps(args.warmup)
     barrier()
 
     # ------------------------------------------------------------ timed region
@@ -508,8 +520,7 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for _ in range(args.steps):
-        one_step()
+    run_steps(args.steps)
     ev1.record(stream)
     barrier()
     ms = ev0.elapsed_time(ev1)
@@ -526,8 +537,7 @@ def main():
         nt = max(20, args.steps // 5)
         for ph in range(5):
             h.kernel_time(reset=True, phase=ph)
-        for _ in range(nt):
-            one_step()
+        run_steps(nt)
         barrier()
         phase_avg = []
         for ph in range(5):
@@ -718,6 +728,7 @@ def main():
         if learner:
             line["config"]["learner"] = args.config
             line["config"]["batch"] = cfg["batch"]
+            line["config"]["rounds_per_call"] = args.rounds_per_call
             line["config"]["l2"] = "L2-resident working set: roofline is effective (L2) bandwidth"
         if args.config == "MLP" and mode == "fused":
             # the round is ONE cooperative kernel (learner gradient + fused update,
@@ -726,13 +737,16 @@ def main():
             bsz, hid, ind, ncls = cfg["batch"], 256, 784, 10
             flops = r * (4 * bsz * ind * hid + 6 * bsz * hid * ncls)
             fused = launches == args.steps
+            multi = args.rounds_per_call > 1 and launches < args.steps
             ms_k = kern_avg if fused else ms_max / args.steps
             mhz = clk.get("sm_mhz") or 1965.0
             peak_tf = 148 * 4 * 32 / 2 * 2 * mhz * 1e6 / 1e12
             ach = flops / (ms_k * 1e-3) / 1e12
             line["roofline"] = {
                 "bound": "alu", "kernel": "mlp_round_kernel<TU, true>" if fused else
-                "5-kernel MLP learner + replica kernel (whole round)",
+                (f"mlp_round_kernel<TU, true>, {launches} launches for {args.steps} rounds "
+                 "(the rounds of one epoch per launch); per-round time = window / K" if multi else
+                 "5-kernel MLP learner + replica kernel (whole round)"),
                 "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf,
                 "traffic": None, "flops_per_launch": flops, "avg_launch_ms": ms_k,
                 "peak_source": "derived: 148 SMs x 4 SMSPs x 32 lanes / FFMA reciprocal "

@@ -367,6 +367,20 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* cuda_stream);
  * opt-in).  Errors: as sma_learner_grads and sma_step. */
 sma_status sma_learner_step(sma_handle* h, int64_t round, void* cuda_stream);
 
+/* Rounds round0, round0 + 1, ..., round0 + count - 1 with the learner in the
+ * loop: the same results as sma_learner_step called for each of them in turn
+ * (bitwise).  For the MLP learner on a single-GPU handle (n = 1, no
+ * MATERIALIZE_C, no CUDA graph) the rounds of one epoch (R10) run
+ * in ONE launch of the fused kernel: the CTA that owns a learner's block of
+ * hidden units keeps that block's weights on chip across the rounds and
+ * prefetches the next round's batch rows and z block, and the rounds are
+ * ordered by per-CTA flags instead of kernel boundaries; a new epoch starts a
+ * new launch.  Every other configuration calls sma_learner_step per round.
+ * Enqueued on cuda_stream; no host synchronisation.  count = 0 is a no-op.
+ * Errors: INVALID_ARG (round0 < 0, count < 0, n_samples < k * batch), STATE
+ * (no learner attached), CUDA, and sma_step's. */
+sma_status sma_learner_steps(sma_handle* h, int64_t round0, int32_t count, void* cuda_stream);
+
 /* ------------------------------------------------ bookkeeping (host only) */
 /* Pure functions of their arguments; no device, no handle (bit-exact with
  * the oracle's independent implementation). */

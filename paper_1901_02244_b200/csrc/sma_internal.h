@@ -116,17 +116,20 @@ cudaError_t launch_mlp_grad(const float* X, const int32_t* y, const int32_t* per
                             cudaStream_t s);
 // SMA_MLP_TC as parsed: -1 unset (per-r defaults), else bits 1 = layer 1, 2 = dW1.
 int mlp_tc_policy();
-// The MLP learner as ONE persistent cooperative kernel (sma_learner_mlp_fused.cu):
-// the gradient of all r local learners into G and, with update = true, the
-// fused n = 1 round (a3-a7) over every parameter.  PL: scratch of
-// num_sms x 16 x 32 floats; bar: 2 zeroed words (grid barrier).  Returns
-// cudaErrorNotSupported (nothing launched) outside its shapes or when disabled
-// (SMA_MLP_FUSED=0, or SMA_MLP_TC set: the five-kernel GEMM paths).
+// The MLP learner as ONE kernel (sma_learner_mlp_fused.cu): the gradient of all
+// r local learners into G and, with update = true, the fused n = 1 round
+// (a3-a7) over every parameter, for `count` consecutive rounds of one epoch
+// (count > 1 only with update; batch rows of round i at perm[pos0 + i kb + ...]).
+// PL: scratch of 2 x num_sms x (16 x 32 + 32) floats; bar: 3 x num_sms zeroed 128-byte
+// flag lines; epoch: the first round's number, above every earlier launch's
+// (the caller adds count).  Returns cudaErrorNotSupported (nothing launched)
+// outside its shapes or when disabled (SMA_MLP_FUSED=0, or SMA_MLP_TC set: the
+// five-kernel GEMM paths).
 bool mlp_fused_enabled();
 cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* perm, int64_t pos0,
-                             int b, int in_dim, int hidden, int classes, int j0, float* PL,
-                             unsigned* bar, unsigned epoch, float* G, const ReplicaArgs& a,
-                             bool update, int num_sms, cudaStream_t s);
+                             int64_t kb, int count, int b, int in_dim, int hidden, int classes,
+                             int j0, float* PL, unsigned* bar, unsigned epoch, float* G,
+                             const ReplicaArgs& a, bool update, int num_sms, cudaStream_t s);
 // MLP layer 1 on tcgen05 (3xTF32 + |.| bound MMAs, cluster K-split); returns
 // cudaErrorNotSupported without launching when the shape is outside its path.
 cudaError_t launch_mlp_hidden_tc(const float* X, const int32_t* perm, int64_t pos0, int b,

@@ -19,6 +19,7 @@
 #include <string.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <cmath>
 #include <functional>
 #include <future>
@@ -139,8 +140,8 @@ struct sma_handle {
   float2* mlp_A1 = nullptr;  // MLP scratch, sized for SMA_MAX_LOCAL_REPLICAS learners
   float* mlp_DA = nullptr;
   float* mlp_E = nullptr;
-  float* mlp_PL = nullptr;     // fused MLP round: partial logits [num_sms][16][32]
-  unsigned* mlp_bar = nullptr; // fused MLP round: flag lines [2 num_sms][32]
+  float* mlp_PL = nullptr;     // fused MLP round: partial logits [2][num_sms][16][32], b2 [2][num_sms][32]
+  unsigned* mlp_bar = nullptr; // fused MLP round: flag lines [3 num_sms][32]
   unsigned mlp_epoch = 0;      // fused MLP round: launches so far (the flags' epoch)
   const float* X = nullptr;
   const int32_t* y = nullptr;
@@ -1255,9 +1256,11 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
       cudaFree(h->mlp_E);
       h->mlp_E = nullptr;
       CUDA_TRY(cudaMalloc(&h->mlp_E, sizeof(float) * (size_t)SMA_MAX_LOCAL_REPLICAS * batch * classes));
-      if (!h->mlp_PL) CUDA_TRY(cudaMalloc(&h->mlp_PL, sizeof(float) * (size_t)h->num_sms * 16 * 32));
-      if (!h->mlp_bar) {  // two kinds of 128-byte flag lines, one per CTA (grid <= #SMs)
-        const size_t nb = sizeof(unsigned) * 32 * 2 * (size_t)h->num_sms;
+      if (!h->mlp_PL)  // two round-parity sets of partial logits (one [16][32] tile per CTA),
+                       // then two of b2 per learner ([32] each; r <= grid <= #SMs)
+        CUDA_TRY(cudaMalloc(&h->mlp_PL, sizeof(float) * 2 * (size_t)h->num_sms * (16 * 32 + 32)));
+      if (!h->mlp_bar) {  // three kinds of 128-byte flag lines, one per CTA (grid <= #SMs)
+        const size_t nb = sizeof(unsigned) * 32 * 3 * (size_t)h->num_sms;
         CUDA_TRY(cudaMalloc(&h->mlp_bar, nb));
         CUDA_TRY(cudaMemset(h->mlp_bar, 0, nb));
       }
@@ -1341,9 +1344,10 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
     a.W = h->W;
     a.ld = h->d_pad;
     a.r = h->r;
-    cudaError_t e = launch_mlp_round(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim,
-                                     h->hidden, h->classes, h->j0, h->mlp_PL, h->mlp_bar, ++h->mlp_epoch, h->G, a,
-                                     false, h->num_sms, s);
+    cudaError_t e = launch_mlp_round(h->X, h->y, h->perm_dev[buf], pos0, (int64_t)h->cfg.k * h->batch,
+                                     1, h->batch, h->in_dim, h->hidden, h->classes, h->j0, h->mlp_PL,
+                                     h->mlp_bar, h->mlp_epoch + 1, h->G, a, false, h->num_sms, s);
+    if (e != cudaErrorNotSupported) ++h->mlp_epoch;
     if (e == cudaErrorNotSupported) {  // the five-kernel path
       CUDA_TRY(launch_mlp_grad(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim, h->hidden,
                                h->classes, h->W, h->d_pad, h->r, h->j0, h->mlp_A1, h->mlp_E,
@@ -1357,6 +1361,86 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
   for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
   leave_staged_set(h);
   return mark_done(h, s);
+}
+
+// The n = 1 MLP round in the fused kernel (sma_learner_mlp_fused.cu) applies.
+static bool mlp_fused_ok(const sma_handle* h) {
+  return h->kind == 1 && !h->collective && !h->matc && h->r > 0 && !(h->graphs && !h->timing) &&
+         mlp_fused_enabled();
+}
+
+// Rounds [round0, round0 + count) of ONE epoch, with the learner in the loop,
+// in one launch of the fused MLP kernel.  *unsupported (nothing enqueued) when
+// the kernel does not cover the shape or count.
+static sma_status fused_mlp_rounds(sma_handle* h, int64_t round0, int count, cudaStream_t s,
+                                   bool* unsupported) {
+  *unsupported = false;
+  DeviceGuard guard(h->dev);
+  int buf = 0;
+  int64_t pos0 = 0;
+  STATUS_TRY(learner_batch(h, round0, s, &buf, &pos0));
+  ReplicaArgs a{};
+  a.W = h->W;
+  a.ld = h->d_pad;
+  a.r = h->r;
+  a.d = h->cfg.d;
+  a.n4 = h->n4;
+  a.z = h->z();
+  a.zprev_next = h->zprev();
+  a.alpha = h->alpha;
+  a.gamma = h->gamma;
+  a.mu = h->mu;
+  a.nonfinite = h->check ? h->nonfinite : nullptr;
+  STATUS_TRY(pre_round(h, s, true));
+  if (count > 1 && h->zread_pending[h->cur]) {  // round 2 of the launch rewrites z[cur] too
+    CUDA_TRY(cudaStreamWaitEvent(s, h->evZread[h->cur], 0));
+    h->zread_pending[h->cur] = false;
+  }
+  cudaEvent_t* tp = nullptr;
+  STATUS_TRY(timer_pair(h, SMA_PHASE_REPLICA, &tp));
+  if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
+  const cudaError_t e =
+      launch_mlp_round(h->X, h->y, h->perm_dev[buf], pos0, (int64_t)h->cfg.k * h->batch, count,
+                       h->batch, h->in_dim, h->hidden, h->classes, h->j0, h->mlp_PL, h->mlp_bar,
+                       h->mlp_epoch + 1, h->G, a, true, h->num_sms, s);
+  if (e == cudaErrorNotSupported) {
+    if (tp) h->tused[SMA_PHASE_REPLICA] -= 2;  // nothing launched: drop the event pair
+    *unsupported = true;
+    return SMA_OK;
+  }
+  CUDA_TRY(e);
+  if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
+  h->mlp_epoch += (unsigned)count;
+  h->launches += 1;
+  for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
+  leave_staged_set(h);
+  for (int i = 0; i < count; ++i) advance(h);
+  return mark_done(h, s);
+}
+
+sma_status sma_learner_steps(sma_handle* h, int64_t round0, int32_t count, void* stream) {
+  if (!h) return fail(SMA_ERR_INVALID_ARG, "NULL handle");
+  NvtxRange nvtx("sma_learner_steps");
+  if (!h->learner) return fail(SMA_ERR_STATE, "no learner attached");
+  if (round0 < 0 || count < 0) return fail(SMA_ERR_INVALID_ARG, "round0 < 0 or count < 0");
+  int64_t i = round0;
+  const int64_t end = round0 + count;
+  const char* fe = getenv("SMA_LEARNER_FUSE");
+  if (!(fe && fe[0] == '1') && mlp_fused_ok(h)) {
+    const int64_t E = h->n_samples / ((int64_t)h->cfg.k * h->batch);
+    if (E < 1)
+      return fail(SMA_ERR_INVALID_ARG, "n_samples=%lld < k*batch: no full round per epoch",
+                  (long long)h->n_samples);
+    while (i < end) {  // one launch per epoch segment (one permutation per launch)
+      const int64_t n = std::min<int64_t>(end - i, E - i % E);
+      bool unsupported = false;
+      STATUS_TRY(fused_mlp_rounds(h, i, (int)n, (cudaStream_t)stream, &unsupported));
+      if (unsupported) break;
+      i += n;
+    }
+  }
+  for (; i < end; ++i) STATUS_TRY(sma_learner_step(h, i, stream));  // one round at a time
+  return SMA_OK;
 }
 
 sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
@@ -1390,44 +1474,12 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
     advance(h);
     return mark_done(h, s);
   }
-  if (!fusable && h->kind == 1 && !h->collective && !h->matc && h->r > 0 &&
-      !(h->graphs && !h->timing) && mlp_fused_enabled()) {
+  if (!fusable && mlp_fused_ok(h)) {
     // n = 1 MLP round: gradient of every local learner and the fused update of
-    // the replicas and z in ONE cooperative kernel (sma_learner_mlp_fused.cu)
-    DeviceGuard guard(h->dev);
-    cudaStream_t s = (cudaStream_t)stream;
-    int buf = 0;
-    int64_t pos0 = 0;
-    STATUS_TRY(learner_batch(h, round, s, &buf, &pos0));
-    ReplicaArgs a{};
-    a.W = h->W;
-    a.ld = h->d_pad;
-    a.r = h->r;
-    a.d = h->cfg.d;
-    a.n4 = h->n4;
-    a.z = h->z();
-    a.zprev_next = h->zprev();
-    a.alpha = h->alpha;
-    a.gamma = h->gamma;
-    a.mu = h->mu;
-    a.nonfinite = h->check ? h->nonfinite : nullptr;
-    STATUS_TRY(pre_round(h, s, true));
-    cudaEvent_t* tp = nullptr;
-    STATUS_TRY(timer_pair(h, SMA_PHASE_REPLICA, &tp));
-    if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
-    const cudaError_t e = launch_mlp_round(h->X, h->y, h->perm_dev[buf], pos0, h->batch, h->in_dim,
-                                           h->hidden, h->classes, h->j0, h->mlp_PL, h->mlp_bar,
-                                           ++h->mlp_epoch, h->G, a, true, h->num_sms, s);
-    if (e != cudaErrorNotSupported) {
-      CUDA_TRY(e);
-      if (tp) CUDA_TRY(cudaEventRecord(tp[1], s));
-      h->launches += 1;
-      for (int i = 0; i < h->r; ++i) set_gptr(h, i, h->G + (int64_t)i * h->d_pad);
-      leave_staged_set(h);
-      advance(h);
-      return mark_done(h, s);
-    }
-    if (tp) h->tused[SMA_PHASE_REPLICA] -= 2;  // nothing launched: drop the event pair
+    // the replicas and z in ONE kernel (sma_learner_mlp_fused.cu)
+    bool unsupported = false;
+    STATUS_TRY(fused_mlp_rounds(h, round, 1, (cudaStream_t)stream, &unsupported));
+    if (!unsupported) return SMA_OK;
   }
   if (!fusable) {  // the same result through the two public calls
     STATUS_TRY(sma_learner_grads(h, round, stream));

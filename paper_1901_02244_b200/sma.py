@@ -48,7 +48,7 @@ EXPORTS = ["sma_create", "sma_destroy", "sma_set_learner_grads", "sma_set_learne
            "sma_step_local", "sma_autotune_step", "sma_set_local_replicas", "sma_learner_step",
            "sma_p2p_handle", "sma_p2p_connect", "sma_set_alpha_global", "sma_get_reference",
            "sma_set_reference", "sma_set_timing", "sma_stage_grads_host",
-           "sma_get_central_async", "sma_synchronize"]
+           "sma_get_central_async", "sma_synchronize", "sma_learner_steps"]
 
 
 class SmaError(RuntimeError):
@@ -111,6 +111,7 @@ def load():
         "sma_autotune_step": ([i32, C.c_double, P, P, P], st),
         "sma_set_local_replicas": ([P, i32, P], st),
         "sma_learner_step": ([P, i64, P], st),
+        "sma_learner_steps": ([P, i64, i32, P], st),
         "sma_p2p_handle": ([P, P], st),
         "sma_p2p_connect": ([P, P], st),
         "sma_set_alpha_global": ([P, C.c_float], st),
@@ -283,6 +284,10 @@ def sma_learner_grads(h: int, rnd: int, stream=None) -> None:
 
 def sma_learner_step(h: int, rnd: int, stream=None) -> None:
     _check(load().sma_learner_step(h, rnd, _stream(stream)), "sma_learner_step")
+
+
+def sma_learner_steps(h: int, rnd0: int, count: int, stream=None) -> None:
+    _check(load().sma_learner_steps(h, rnd0, count, _stream(stream)), "sma_learner_steps")
 
 
 def sma_p2p_handle(h: int) -> bytes:

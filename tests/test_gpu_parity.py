@@ -705,6 +705,85 @@ def test_paper_config_sizes_sampled_parity(torch_cuda, S, orc, cfg):
     h.close()
 
 
+@pytest.mark.parametrize("k", [4, 8, 16, 32])
+def test_mlp_learner_steps_multi_round_bitwise(torch_cuda, S, orc, k):
+    """sma_learner_steps (the rounds of one epoch in ONE launch of the fused MLP
+    kernel: weights kept on chip across rounds, next batch / z block
+    prefetched, rounds ordered by per-CTA flags) is bitwise equal to
+    sma_learner_step called once per round -- itself checked against the fp64
+    oracle round by round (test_mlp_bench_configs_per_round_100_rounds) -- over
+    40 rounds crossing epoch boundaries (2,000 samples: E = 31 / 15 / 7 / 3
+    rounds per epoch at k = 4 / 8 / 16 / 32), split over two calls.  k = 32 has
+    no multi-round launch (its block's W1 rows do not fit on chip) and must
+    fall back to one launch per round."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(2_000, seed=21)
+    b, R, cut = 16, 40, 13
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    w0 = np.random.default_rng(6).normal(0, 0.05, MLP_D).astype(np.float32)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    hs, launches = [], []
+    for multi in (False, True):
+        h = S.Sma(MLP_D, k, a, g, m, w0)
+        S.sma_learner_attach(h.h, 1, 784, 256, 10, b, Xd, yd, X.shape[0], 7)
+        s = torch.cuda.Stream()
+        l0 = h.launch_count()
+        if multi:
+            S.sma_learner_steps(h.h, 0, cut, s)
+            S.sma_learner_steps(h.h, cut, R - cut, s)
+            S.sma_learner_steps(h.h, R, 0, s)   # count = 0: no-op
+        else:
+            for i in range(R):
+                S.sma_learner_step(h.h, i, s)
+        s.synchronize()
+        launches.append(h.launch_count() - l0)
+        hs.append(h)
+    E = X.shape[0] // (k * b)
+    assert launches[0] == R
+    if k < 32:   # one launch per epoch segment of each call
+        segs = sum(len({i // E for i in range(lo, hi)}) for lo, hi in ((0, cut), (cut, R)))
+        assert launches[1] == segs, (launches, segs)
+    else:
+        assert launches[1] == R
+    assert np.array_equal(hs[0].central(), hs[1].central())
+    assert np.array_equal(hs[0].central_prev(), hs[1].central_prev())
+    for j in range(k):
+        assert np.array_equal(hs[0].replica(j), hs[1].replica(j)), j
+    with pytest.raises(S.SmaError):
+        S.sma_learner_steps(hs[1].h, 0, -1, None)
+    for h in hs:
+        h.close()
+
+
+def test_learner_steps_softmax_is_per_round(torch_cuda, S, orc):
+    """sma_learner_steps on the softmax learner (no multi-round kernel) equals
+    sma_learner_step per round bitwise, and the oracle within the bar (C1)."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(3_000, seed=4)
+    k, b, R = 4, 16, 50
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    hs = []
+    for multi in (False, True):
+        h = S.Sma(7850, k, a, g, m, np.zeros(7850, np.float32))
+        S.sma_learner_attach(h.h, 0, 784, 0, 10, b, Xd, yd, X.shape[0], 99)
+        s = torch.cuda.Stream()
+        if multi:
+            S.sma_learner_steps(h.h, 0, R, s)
+        else:
+            for i in range(R):
+                S.sma_learner_step(h.h, i, s)
+        s.synchronize()
+        hs.append(h)
+    assert np.array_equal(hs[0].central(), hs[1].central())
+    for j in range(k):
+        assert np.array_equal(hs[0].replica(j), hs[1].replica(j))
+    zr, _, _ = orc.run_softmax(X, y, b, 99, k, a, g, m, R, np.zeros(7850))
+    assert relerr(hs[1].central(), zr) <= TOL
+    for h in hs:
+        h.close()
+
+
 def test_learner_step_fused_matches_unfused(torch_cuda, S, orc):
     """sma_learner_step's fused softmax round vs sma_learner_grads + sma_step
     over 60 rounds crossing an epoch, to 1e-6 (not bitwise: the fused kernel sums
