@@ -74,6 +74,15 @@ def parse():
                     help="learner configs: rounds per sma_learner_steps call (the MLP learner "
                          "then runs the rounds of one epoch in one launch of its fused kernel); "
                          "1 = one sma_learner_step per round")
+    ap.add_argument("--emulate-n", type=int, default=0,
+                    help="measurement only, 1 GPU with --force-collective --zsync p2p: the 1-rank "
+                         "z-sync moves the HBM traffic ONE GPU of an N-rank job sees (whole partial "
+                         "read, whole z written, z/z_prev read on 1/N) while the replica kernel of "
+                         "r = k/N replicas runs -- the per-GPU load of N GPUs (SMA_P2P_EMULATE_N); "
+                         "the z it computes is wrong, so the line is not a bench value")
+    ap.add_argument("--emulate-ctas", type=int, default=0,
+                    help="with --emulate-n: cap the z-sync grid (SMA_P2P_CTAS) to pace its traffic "
+                         "like the NVLink-bound real one")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -346,6 +355,10 @@ def workload_name(cfg, d, k):
 
 def main():
     args = parse()
+    if args.emulate_n:
+        os.environ["SMA_P2P_EMULATE_N"] = str(args.emulate_n)
+        if args.emulate_ctas:
+            os.environ["SMA_P2P_CTAS"] = str(args.emulate_ctas)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -721,6 +734,17 @@ def main():
                                                  "multi-GPU measurement")
         if e2e:
             line["e2e"] = e2e
+        if args.emulate_n:
+            n_e = args.emulate_n
+            line["config"]["emulated_n"] = n_e
+            line["config"]["emulated_zsync_ctas"] = args.emulate_ctas or None
+            line["config"]["note_emulation"] = (
+                f"MEASUREMENT ONLY (not a bench value; the z it computes is wrong): one GPU runs "
+                f"the replica kernel of r = k/{n_e} replicas over the full vector and, in Mode B "
+                f"concurrently, a 1-rank z-sync that moves the HBM traffic one GPU of a "
+                f"{n_e}-rank job sees: the whole partial read ({4 * d_pad} B), the whole z[1-cur] "
+                f"written ({4 * d_pad} B), z and z_prev read on 1/{n_e} ({8 * d_pad // n_e} B); "
+                f"its NVLink pacing is approximated by capping its grid (emulated_zsync_ctas)")
         if args.tau != 1:
             line["config"]["tau"] = args.tau
             line["config"]["note"] = ("E11 analog (P:1476-1503): iterations/s with "
@@ -755,7 +779,8 @@ def main():
                 "note": "FLOPs = r (4 b in_dim hidden + 6 b hidden classes): layer 1, dW1, "
                         "logits, dW2, da1; the per-learner GEMMs are 16 x 784 x 256 -- a chain "
                         "of dependent phases, latency-bound, not FLOP-bound",
-                "timing": timing_src}
+                "timing": timing_src if fused else "timed window / K (CUDA events on the launching "
+                                                   "stream around the K rounds)"}
         if not args.no_cpu_baseline and not learner:
             line["cpu_baseline"] = cpu_baseline(d, k, alpha, gamma, mu)
         print(json.dumps(line), flush=True)

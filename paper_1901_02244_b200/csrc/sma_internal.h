@@ -189,6 +189,7 @@ struct P2PArgs {
                          // [3] barrier A passed (device-scope flag set by CTA 0)
   int* nonfinite;
   int push;              // SMA_FLAG_P2P_PUSH: the partials are already in local slots
+  int emu_n;             // SMA_P2P_EMULATE_N (measurement only, 1 rank): 0 = off, else see sma_p2p.cu
 };
 cudaError_t launch_zsync_p2p(int mode, const P2PArgs& a, int num_ctas, cudaStream_t s);
 

@@ -154,6 +154,14 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
     return a.push ? mine + (int64_t)g * shard + (e - soff)
                   : reinterpret_cast<const float*>(a.base[g] + a.off_part) + e;
   };
+  // SMA_P2P_EMULATE_N = N on a 1-rank handle (bench.py --emulate-n; measurement
+  // only, the z it produces is WRONG outside the first 1/N of the vector): the
+  // kernel moves the HBM traffic that ONE GPU of an N-rank job sees -- its whole
+  // partial read (its own shard by itself, the others by the peers' loads), the
+  // whole z[1-cur] written (every owner's all-gather stores land here), but z and
+  // z_prev read only on its own 1/N shard -- so the overlapped replica kernel can
+  // be measured against that load on one GPU.
+  const int64_t own4 = a.emu_n ? a.len4 / a.emu_n : a.len4;
   // two chunks per iteration: 2n peer loads + 4 local loads in flight
   int64_t c = (int64_t)blockIdx.x * kP2PThreads + threadIdx.x;
   for (; c + stride < a.len4; c += 2 * stride) {
@@ -166,8 +174,10 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
       s1.x = __fadd_rn(s1.x, v1.x); s1.y = __fadd_rn(s1.y, v1.y);
       s1.z = __fadd_rn(s1.z, v1.z); s1.w = __fadd_rn(s1.w, v1.w);
     }
-    const float4 zn0 = shard_update<MODE>(ld_ro4(zl + e0), s0, ld_rw4(zpl + e0), a);  // a7
-    const float4 zn1 = shard_update<MODE>(ld_ro4(zl + e1), s1, ld_rw4(zpl + e1), a);
+    const float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool o0 = c < own4, o1 = c + stride < own4;
+    const float4 zn0 = shard_update<MODE>(o0 ? ld_ro4(zl + e0) : f0, s0, o0 ? ld_rw4(zpl + e0) : f0, a);  // a7
+    const float4 zn1 = shard_update<MODE>(o1 ? ld_ro4(zl + e1) : f0, s1, o1 ? ld_rw4(zpl + e1) : f0, a);
     for (int g = 0; g < n; ++g) {  // a8: broadcast the updated shard chunks
       float* zg = reinterpret_cast<float*>(a.base[g] + a.off_zprev);
       st4(zg + e0, zn0);
@@ -184,7 +194,9 @@ __global__ void __launch_bounds__(kP2PThreads) zsync_p2p_kernel(const P2PArgs a)
       sum.x = __fadd_rn(sum.x, v.x); sum.y = __fadd_rn(sum.y, v.y);
       sum.z = __fadd_rn(sum.z, v.z); sum.w = __fadd_rn(sum.w, v.w);
     }
-    const float4 zn = shard_update<MODE>(ld_ro4(zl + e), sum, ld_rw4(zpl + e), a);
+    const float4 f0 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool o = c < own4;
+    const float4 zn = shard_update<MODE>(o ? ld_ro4(zl + e) : f0, sum, o ? ld_rw4(zpl + e) : f0, a);
     for (int g = 0; g < n; ++g) st4(reinterpret_cast<float*>(a.base[g] + a.off_zprev) + e, zn);
     bad |= !(isfinite(zn.x) && isfinite(zn.y) && isfinite(zn.z) && isfinite(zn.w));
   }

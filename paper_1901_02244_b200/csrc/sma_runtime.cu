@@ -443,6 +443,13 @@ sma_status enqueue_zsync(sma_handle* h, int mode, const float* partial, float co
     a.ctl = h->p2p_ctl;
     a.nonfinite = h->check ? h->nonfinite : nullptr;
     a.push = h->push ? 1 : 0;
+    // SMA_P2P_EMULATE_N=N (measurement only; ignored unless world == 1): see sma_p2p.cu
+    static const int emu_n = [] {
+      const char* e = getenv("SMA_P2P_EMULATE_N");
+      const int v = e ? atoi(e) : 0;
+      return v >= 2 && v <= kMaxP2PRanks ? v : 0;
+    }();
+    a.emu_n = h->cfg.world == 1 ? emu_n : 0;
     STATUS_TRY(timer_pair(h, SMA_PHASE_FUSED_ZSYNC, &tp));
     if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
     // persistent grid: SMA_P2P_CTAS_PER_SM x #SMs CTAs (default 4); in Mode B
