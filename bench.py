@@ -40,6 +40,13 @@ METRIC = ("SMA rounds/sec and HBM/NVLink GB/s vs peak at ResNet-50 size, k repli
 UNIT = "rounds/s"
 HBM_FALLBACK_GBS = 6650.0
 NVLINK_PEAK_GBS = 770.0   # measured per-direction peer bandwidth (B200_PROFILING.md)
+# L2-resident rounds (C1-C3, the learners): the L2 slice (LTS) throughput cap of
+# /opt/skills/guides/B300_MICROARCH.md ("~6300 B/cyc full-chip", measured on B300)
+# x the B200's 1,965 MHz max SM clock.  torch's own L2-resident copy / add kernels
+# reach 8.2 / 9.2 TB/s on this B200 (profiles/r02_l2_bw.json), below our replica
+# kernel at C3, so the guide's cap is the denominator.
+L2_PEAK_GBS = 6300 * 1.965
+L2_BYTES = 126 * (1 << 20)
 
 
 def parse():
@@ -268,8 +275,20 @@ def arm_config(args, world, d, d_pad, k, alpha, gamma, mu, zsync=None, push=Fals
             "materialize_c": bool(args.matc), "hierarchical": bool(args.hier),
             "parallelism": f"sma-dp{world}" + ("" if not collective else f"+{zsync}-zsync") +
                            ("-push" if push else ""),
-            "l2": "no flush: per-round working set "
-                  f"{(alg_bytes / 1e9):.2f} GB/GPU >> 126 MB L2"}
+            "l2": l2_note(d_pad, r)}
+
+
+def working_set(d_pad, r):
+    """Bytes a round touches per GPU: r replicas + r gradients + z and z_prev."""
+    return 4 * d_pad * (2 * r + 2)
+
+
+def l2_note(d_pad, r):
+    ws = working_set(d_pad, r)
+    if ws > L2_BYTES:
+        return f"no flush: per-round working set {ws / 1e9:.2f} GB/GPU >> 126 MB L2"
+    return (f"L2-resident: per-round working set {ws / 1e6:.1f} MB/GPU < 126 MB L2, not flushed "
+            "(the rounds of a training loop reuse it); roofline against the L2 throughput cap")
 
 
 def nvlink_counters(device):
@@ -721,7 +740,15 @@ def main():
                          "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                          "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": kern_avg,
                          "peak_source": peak_src, "vs_8TBs_spec": achieved / 8000.0,
-                         "timing": timing_src},
+                         "timing": timing_src} if working_set(d_pad, r) > L2_BYTES else
+                        {"bound": "l2", "kernel": kname, "achieved": achieved,
+                         "peak": L2_PEAK_GBS, "unit": "GB/s", "frac": achieved / L2_PEAK_GBS,
+                         "traffic": traffic, "alg_bytes_per_launch": alg_bytes,
+                         "avg_launch_ms": kern_avg,
+                         "peak_source": "derived: B300_MICROARCH.md L2 (LTS) throughput cap "
+                                        "~6300 B/cycle x 1965 MHz; torch's L2-resident copy/add "
+                                        "reach 8.2/9.2 TB/s here (profiles/r02_l2_bw.json)",
+                         "vs_hbm_peak": achieved / peak, "timing": timing_src},
             "gpu_launches": launches_total,
             "clocks": clk,
         }
@@ -753,7 +780,8 @@ def main():
             line["config"]["learner"] = args.config
             line["config"]["batch"] = cfg["batch"]
             line["config"]["rounds_per_call"] = args.rounds_per_call
-            line["config"]["l2"] = "L2-resident working set: roofline is effective (L2) bandwidth"
+            line["config"]["l2"] = ("L2-resident working set (replicas, gradients, z and the "
+                                    "dataset's batch rows): not flushed")
         if args.config == "MLP" and mode == "fused":
             # the round is ONE cooperative kernel (learner gradient + fused update,
             # sma_learner_mlp_fused.cu) unless SMA_MLP_FUSED=0 / SMA_MLP_TC force the
