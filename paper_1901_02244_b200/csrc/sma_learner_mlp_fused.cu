@@ -351,11 +351,15 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
       // ---- phase 1: a1 = W1 x + b1 for (16 rows x U units), chunk by chunk
       for (int ch = 0; ch < nch; ++ch) {
         if (i == 0) bulk::wait(&mbar[2], ch & 1);
-        {
+        // K is always split into kWarps slices (summed in slice order below), each
+        // group-1 warp taking slices warp, warp + nw1, ...: a1's rounding does not
+        // depend on the group sizes, so one round per launch (2 group-2 warps)
+        // and several (4) give the same bits
+        for (int sl = warp; sl < kWarps; sl += nw1) {
           const int rg = lane >> 2, ug = lane & 3;  // 8 row groups x 4 unit groups
           const int t0 = rg * kTR;
           const int n4k = in_dim >> 2;
-          const int k4a = warp * n4k / nw1, k4b = (warp + 1) * n4k / nw1;
+          const int k4a = sl * n4k / kWarps, k4b = (sl + 1) * n4k / kWarps;
           float acc[kTR][TU];
   #pragma unroll
           for (int u = 0; u < TU; ++u) {
@@ -386,7 +390,7 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
           for (int u = 0; u < TU; ++u) {
             const int ul = ug + kUG * u;
   #pragma unroll
-            for (int q = 0; q < kTR; ++q) part[(warp * kRows + t0 + q) * CU + ul] = acc[q][u];
+            for (int q = 0; q < kTR; ++q) part[(sl * kRows + t0 + q) * CU + ul] = acc[q][u];
           }
         }
         for (int ul = warp; ul < CU; ul += nw1) {  // ||W1[u]|| (one warp per unit, fixed order)
@@ -406,7 +410,7 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
         for (int q = tid; q < kRows * CU; q += nt1) {  // cross-warp sum, bias, certainty test
           const int t = q / CU, ul = q - t * CU;
           float s = 0.f;
-          for (int w = 0; w < nw1; ++w) s = __fadd_rn(s, part[(w * kRows + t) * CU + ul]);
+          for (int w = 0; w < kWarps; ++w) s = __fadd_rn(s, part[(w * kRows + t) * CU + ul]);
           const float bias = b1s[uc + ul];
           const float av = __fadd_rn(s, bias);
           // |fl(a) - a| <= ~110 u (sum |w x| + |b|) << 2^-12 (||w|| ||x|| + |b|)
