@@ -32,6 +32,8 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <cooperative_groups.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -45,6 +47,10 @@ namespace sma {
 namespace {
 constexpr int kThr = 256;
 constexpr int kWarps = kThr / 32;
+// Phase 1 splits K into kSlices slices (partials summed in slice order): 12 is
+// a multiple of the group-1 sizes 4 and 6, so the slices spread evenly, and a1's
+// rounding does not depend on how many warps run phase 1.
+constexpr int kSlices = 12;
 constexpr int kRows = 16;        // batch rows per learner (b <= 16, zero-padded)
 constexpr int kTR = 2;           // rows per lane in phase 1 (8 row groups)
 constexpr int kUG = 4;           // unit groups per warp in phase 1
@@ -91,6 +97,14 @@ __device__ __forceinline__ void flag_poll(const unsigned* line, unsigned epoch) 
   while ((int)(ld_acquire_gpu(line) - epoch) < 0)
     if (clock64() - t0 > 60000000000ll) __trap();  // ~30 s: a CTA never arrived
 }
+// Split cluster barrier (every thread of the cluster arrives, then waits):
+// release / acquire at cluster scope, covering shared::cluster and global memory.
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
 // Named barrier over the first / second warp group of the CTA.
 __device__ __forceinline__ void group_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -108,6 +122,8 @@ struct MlpRoundArgs {
   int nx;                 // batch-row buffers: 2 = the next round's rows prefetched
   int nzb;                // z-row buffers of the W1 block: 0 (z read from L2), 1, or 2 (prefetched)
   int nzw;                // UPDATE: warps of group 2 (0 = it runs on all warps, after phase 1)
+  int cl;                 // UPDATE, cluster mode: the r CTAs of one unit block form a thread-block
+                          // cluster (blockIdx.x = blk * r + j) and exchange z through it
   float* PL;              // [2][grid][kRows][classes] partial logits (round parity)
   float* B2;              // [2][r][32] b2^{i+1} of each learner, written by its block 0 (parity)
   float* G;               // gradients [r][ld]
@@ -191,8 +207,8 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
   float* xs = sm;                                        // [nx][kRows][xld]
   float* w1s = xs + m.nx * kRows * xld;                  // [CU][xld] W1 rows (a chunk)
   float* zs = w1s + CU * xld;                            // [nzb][U][xld] z rows
-  float* part = zs + m.nzb * U * xld;                    // [kWarps][kRows][CU]
-  float* hs = part + kWarps * kRows * CU;                // [kRows][U] relu(a1)
+  float* part = zs + m.nzb * U * xld;                    // [kSlices][kRows][CU]
+  float* hs = part + kSlices * kRows * CU;               // [kRows][U] relu(a1)
   float* das = hs + kRows * U;                           // [kRows][U] da1
   float* lg = das + kRows * U;                           // [kRows][32] logits
   float* es = lg + kRows * 32;                           // [kRows][32] softmax - onehot
@@ -212,7 +228,10 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
   // [0], [1] batch-row buffers; [2] weight block; [3], [4] z block buffers; [5] partial logits
   __shared__ __align__(8) uint64_t mbar[6];
 
-  const int j = blockIdx.x / nblk, blk = blockIdx.x - j * nblk;
+  // cluster mode: the r CTAs of unit block blk are one cluster (rank j)
+  const int j = m.cl ? (int)(blockIdx.x % (unsigned)m.a.r) : (int)(blockIdx.x / nblk);
+  const int blk = m.cl ? (int)(blockIdx.x / (unsigned)m.a.r) : (int)(blockIdx.x - j * nblk);
+  const int cid = j * nblk + blk;  // learner-major CTA index (partial logits, their flags)
   const int u0 = blk * U;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const ReplicaArgs& a = m.a;
@@ -300,7 +319,10 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
       bulk::copy(w2s + c * U, W + oW2 + (int64_t)c * hidden + u0, 4u * U, &mbar[2]);
     if (lane == 0) bulk::copy(b1s, W + ob1 + u0, 4u * U, &mbar[2]);
   }
-  if (UPDATE && warp == 0) issue_z_warp(a.z, 0);
+  if (UPDATE && warp == 0) {
+    issue_z_warp(a.z, 0);
+    if (m.cl) issue_z_warp(a.zprev_next, 1);  // cluster mode: z^{-1} too (then z moves through DSMEM)
+  }
 
   bool bad = false;
   const float fb = (float)b;
@@ -314,12 +336,14 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
   const int nzw = UPDATE ? m.nzw : 0;  // group-2 warps (0: none, group 2's work runs on all)
   const int nw1 = kWarps - nzw;
   const int nt1 = 32 * nw1;
-  unsigned long long pacc[PROF ? 16 : 1] = {};
+  __shared__ unsigned long long pacc[16];  // (shared: no register pressure on the PROF build)
+  if (PROF && tid < 16) pacc[tid] = 0;
+  __syncthreads();
   long long tprev = PROF ? clock64() : 0;
   auto pmark = [&](int q) {  // SMA_MLP_PROF cycle accumulators (threads 0 and nt1)
     if (PROF && (tid == 0 || tid == nt1)) {
       const long long t = clock64();
-      pacc[q] += (unsigned long long)(t - tprev);
+      if ((tid == 0) == (q < 12)) pacc[q] += (unsigned long long)(t - tprev);
       tprev = t;
     }
   };
@@ -351,15 +375,15 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
       // ---- phase 1: a1 = W1 x + b1 for (16 rows x U units), chunk by chunk
       for (int ch = 0; ch < nch; ++ch) {
         if (i == 0) bulk::wait(&mbar[2], ch & 1);
-        // K is always split into kWarps slices (summed in slice order below), each
+        // K is always split into kSlices slices (summed in slice order below), each
         // group-1 warp taking slices warp, warp + nw1, ...: a1's rounding does not
         // depend on the group sizes, so one round per launch (2 group-2 warps)
         // and several (4) give the same bits
-        for (int sl = warp; sl < kWarps; sl += nw1) {
+        for (int sl = warp; sl < kSlices; sl += nw1) {
           const int rg = lane >> 2, ug = lane & 3;  // 8 row groups x 4 unit groups
           const int t0 = rg * kTR;
           const int n4k = in_dim >> 2;
-          const int k4a = sl * n4k / kWarps, k4b = (sl + 1) * n4k / kWarps;
+          const int k4a = sl * n4k / kSlices, k4b = (sl + 1) * n4k / kSlices;
           float acc[kTR][TU];
   #pragma unroll
           for (int u = 0; u < TU; ++u) {
@@ -410,7 +434,7 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
         for (int q = tid; q < kRows * CU; q += nt1) {  // cross-warp sum, bias, certainty test
           const int t = q / CU, ul = q - t * CU;
           float s = 0.f;
-          for (int w = 0; w < kWarps; ++w) s = __fadd_rn(s, part[(w * kRows + t) * CU + ul]);
+          for (int w = 0; w < kSlices; ++w) s = __fadd_rn(s, part[(w * kRows + t) * CU + ul]);
           const float bias = b1s[uc + ul];
           const float av = __fadd_rn(s, bias);
           // |fl(a) - a| <= ~110 u (sum |w x| + |b|) << 2^-12 (||w|| ||x|| + |b|)
@@ -459,7 +483,7 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
       }
       pmark(2);
       // partial logits of this unit block
-      float* PL = m.PL + ((int64_t)(i & 1) * gridDim.x + blockIdx.x) * npl;
+      float* PL = m.PL + ((int64_t)(i & 1) * gridDim.x + cid) * npl;
       for (int q = tid; q < npl; q += nt1) {
         const int t = q / classes, c = q - t * classes;
         float s = 0.f;
@@ -468,7 +492,7 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
         PL[q] = s;
       }
       group_sync(1, nt1);
-      if (tid == 0) st_release_gpu(fPL + 32 * blockIdx.x, ep);  // my partial logits are written
+      if (tid == 0) st_release_gpu(fPL + 32 * cid, ep);  // my partial logits are written
       pmark(3);
     }
     // group 2 (UPDATE): with nzw = 0 every warp runs it here, after its partial
@@ -493,74 +517,163 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
           bulk::copy(xs + (((i + 1) & 1) * kRows + lane) * xld, m.X + (int64_t)rows[(i + 1) & 1][lane] * in_dim,
                      rowb, &mbar[(i + 1) & 1]);
       }
-      // ---- z^{i+1} on this CTA's slice, from the pre-update replicas W^i
-      if (i > 0) {  // every CTA has stored W^i
-        for (int c = zt; c < (int)gridDim.x; c += nzt) flag_poll(fP2 + 32 * c, ep - 1u);
-        group_sync(2, nzt);
-      }
-      pmark(12);
-      // z^i of b2 (block 0's update): complete since round i - 1's ZD flags
-      if (blk == 0 && zt < classes) zb2s[zt] = ld_cg(zc + ob2 + zt);
-        const int64_t per = (a.n4 + gridDim.x - 1) / gridDim.x;
-        const int64_t c_lo = (int64_t)blockIdx.x * per;
-        const int64_t c_hi = c_lo + per < a.n4 ? c_lo + per : a.n4;
-        // two columns per thread and iteration, every load of a replica group issued
-        // before its arithmetic (the compiler cannot hoist loads across the stores)
-        const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int64_t c4 = c_lo + zt; c4 < c_hi; c4 += 2 * nzt) {
-          const bool two = c4 + nzt < c_hi;
-          const int64_t p0 = c4 << 2, p1 = (c4 + nzt) << 2;
-          const float4 z0 = ld_z4(zc + p0), zp0 = ld_z4(zo + p0);
-          const float4 z1 = two ? ld_z4(zc + p1) : zero;
-          const float4 zp1 = two ? ld_z4(zo + p1) : zero;
-          float4 s0 = zero, s1 = zero;
-          for (int jj = 0; jj < a.r; jj += 4) {
-            float4 w0[4], w1[4];
-  #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              w0[u] = jj + u < a.r ? ld_z4(a.W + (int64_t)(jj + u) * a.ld + p0) : zero;
-              w1[u] = two && jj + u < a.r ? ld_z4(a.W + (int64_t)(jj + u) * a.ld + p1) : zero;
-            }
-  #pragma unroll
-            for (int u = 0; u < 4; ++u) {  // corrections added in ascending j
-              if (jj + u < a.r) {
-                s0.x = __fadd_rn(s0.x, __fmul_rn(a.alpha, __fsub_rn(w0[u].x, z0.x)));
-                s0.y = __fadd_rn(s0.y, __fmul_rn(a.alpha, __fsub_rn(w0[u].y, z0.y)));
-                s0.z = __fadd_rn(s0.z, __fmul_rn(a.alpha, __fsub_rn(w0[u].z, z0.z)));
-                s0.w = __fadd_rn(s0.w, __fmul_rn(a.alpha, __fsub_rn(w0[u].w, z0.w)));
-                s1.x = __fadd_rn(s1.x, __fmul_rn(a.alpha, __fsub_rn(w1[u].x, z1.x)));
-                s1.y = __fadd_rn(s1.y, __fmul_rn(a.alpha, __fsub_rn(w1[u].y, z1.y)));
-                s1.z = __fadd_rn(s1.z, __fmul_rn(a.alpha, __fsub_rn(w1[u].z, z1.z)));
-                s1.w = __fadd_rn(s1.w, __fmul_rn(a.alpha, __fsub_rn(w1[u].w, z1.w)));
-              }
-            }
+      if (m.cl) {
+        // ---- z^{i+1} on this CTA's 1/r of the unit block, from the cluster
+        // peers' pre-update replicas W^i read from THEIR shared memory (DSMEM):
+        // the block's W1 rows, b1, W2 columns (and b2) live only in the cluster
+        if (i > 0) cluster_wait();  // (P_{i-1}) every peer holds W^i
+        pmark(12);
+        if (i == 0) {  // z^0 and z^{-1} of the block (later rounds: DSMEM stores of the peers)
+          bulk::wait(&mbar[3], 0);
+          bulk::wait(&mbar[4], 0);
+        }
+        namespace cg = cooperative_groups;
+        const cg::cluster_group clu = cg::this_cluster();
+        const int r = a.r, zb = i & 1;
+        const int n4 = in_dim >> 2, nI = U * n4;
+        const int it1 = (j + 1) * nI / r;
+        for (int it = j * nI / r + zt; it < it1; it += nzt) {
+          const int ul = it / n4, f4 = it - ul * n4;
+          const int64_t o = (int64_t)(u0 + ul) * in_dim + 4 * f4;
+          // z^i and z^{i-1} of the block are both on chip (zs[i & 1], zs[(i + 1) & 1])
+          const float4 z0 = reinterpret_cast<const float4*>(zs + (zb * U + ul) * xld)[f4];
+          const float4 zp0 = reinterpret_cast<const float4*>(zs + ((zb ^ 1) * U + ul) * xld)[f4];
+          float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+          for (int l = 0; l < r; ++l) {  // corrections added in ascending learner
+            const float4 w = reinterpret_cast<const float4*>(clu.map_shared_rank(w1s, l) + ul * xld)[f4];
+            s0.x = __fadd_rn(s0.x, __fmul_rn(a.alpha, __fsub_rn(w.x, z0.x)));
+            s0.y = __fadd_rn(s0.y, __fmul_rn(a.alpha, __fsub_rn(w.y, z0.y)));
+            s0.z = __fadd_rn(s0.z, __fmul_rn(a.alpha, __fsub_rn(w.z, z0.z)));
+            s0.w = __fadd_rn(s0.w, __fmul_rn(a.alpha, __fsub_rn(w.w, z0.w)));
           }
           float4 zn;
           zn.x = __fadd_rn(__fadd_rn(z0.x, s0.x), __fmul_rn(a.mu, __fsub_rn(z0.x, zp0.x)));
           zn.y = __fadd_rn(__fadd_rn(z0.y, s0.y), __fmul_rn(a.mu, __fsub_rn(z0.y, zp0.y)));
           zn.z = __fadd_rn(__fadd_rn(z0.z, s0.z), __fmul_rn(a.mu, __fsub_rn(z0.z, zp0.z)));
           zn.w = __fadd_rn(__fadd_rn(z0.w, s0.w), __fmul_rn(a.mu, __fsub_rn(z0.w, zp0.w)));
-          *reinterpret_cast<float4*>(zo + p0) = zn;
+          *reinterpret_cast<float4*>(zo + o) = zn;
+          // z^{i+1} into every peer's zs[(i + 1) & 1] (where z^{i-1} was: each CTA
+          // reads only its own part of it, which only it overwrites)
+          for (int l = 0; l < r; ++l)
+            reinterpret_cast<float4*>(clu.map_shared_rank(zs, l) + ((zb ^ 1) * U + ul) * xld)[f4] = zn;
           bad |= !finite4(zn);
-          if (two) {
-            zn.x = __fadd_rn(__fadd_rn(z1.x, s1.x), __fmul_rn(a.mu, __fsub_rn(z1.x, zp1.x)));
-            zn.y = __fadd_rn(__fadd_rn(z1.y, s1.y), __fmul_rn(a.mu, __fsub_rn(z1.y, zp1.y)));
-            zn.z = __fadd_rn(__fadd_rn(z1.z, s1.z), __fmul_rn(a.mu, __fsub_rn(z1.z, zp1.z)));
-            zn.w = __fadd_rn(__fadd_rn(z1.w, s1.w), __fmul_rn(a.mu, __fsub_rn(z1.w, zp1.w)));
-            *reinterpret_cast<float4*>(zo + p1) = zn;
-            bad |= !finite4(zn);
+        }
+        if (j == 0) {  // the block's W2 columns, b1 (and, block 0, b2): cluster rank 0
+          const int nw2 = classes * U, nsm = nw2 + U + (blk == 0 ? classes : 0);
+          for (int q = zt; q < nsm; q += nzt) {
+            int64_t o;
+            float z0, zp0;
+            const float* src;  // this parameter's slot in a peer's shared memory
+            float* zdst;       // and where z^{i+1} goes in every peer's (nullptr: b2)
+            int so;
+            if (q < nw2) {
+              const int c = q / U, ul = q - c * U;
+              o = oW2 + (int64_t)c * hidden + u0 + ul;
+              z0 = zw2s[zb * 32 * U + q];
+              zp0 = zw2s[(zb ^ 1) * 32 * U + q];
+              src = w2s; so = q;
+              zdst = zw2s + (zb ^ 1) * 32 * U + q;
+            } else if (q < nw2 + U) {
+              const int ul = q - nw2;
+              o = ob1 + u0 + ul;
+              z0 = zb1s[zb * U + ul];
+              zp0 = zb1s[(zb ^ 1) * U + ul];
+              src = b1s; so = ul;
+              zdst = zb1s + (zb ^ 1) * U + ul;
+            } else {
+              const int c = q - nw2 - U;
+              o = ob2 + c;
+              z0 = ld_cg(zc + o);
+              zp0 = ld_cg(zo + o);
+              src = b2s; so = c;
+              zdst = nullptr;
+            }
+            float acc = 0.f;
+            for (int l = 0; l < r; ++l)
+              acc = __fadd_rn(acc, __fmul_rn(a.alpha, __fsub_rn(clu.map_shared_rank(src, l)[so], z0)));
+            const float zn = __fadd_rn(__fadd_rn(z0, acc), __fmul_rn(a.mu, __fsub_rn(z0, zp0)));
+            zo[o] = zn;
+            if (zdst)
+              for (int l = 0; l < r; ++l) *clu.map_shared_rank(zdst, l) = zn;
+            bad |= !isfinite(zn);
           }
         }
+        // z^i of b2 (block 0's update): written by cluster 0 in round i - 1
+        if (blk == 0 && zt < classes) zb2s[zt] = ld_cg(zc + ob2 + zt);
         pmark(13);
-      group_sync(2, nzt);
-      if (zt == 0) st_release_gpu(fZD + 32 * blockIdx.x, ep);  // done reading W^i, z^{i+1} written
-      // every CTA has read W^i (before any replica store) and z^{i+1} is complete
-      for (int c = zt; c < (int)gridDim.x; c += nzt) flag_poll(fZD + 32 * c, ep);
-      group_sync(2, nzt);
-      pmark(14);
-      if (i + 1 < m.count && zw == 0) {  // prefetch round i + 1's z block
-        fence_proxy_async();  // z^{i+1} was written by other CTAs (generic proxy)
-        issue_z_warp(zo, (i + 1) & 1);
+        cluster_arrive();  // (Z_i) my part of z^{i+1} is stored; I have read the peers' W^i
+        pmark(14);
+      } else {
+        // ---- z^{i+1} on this CTA's slice, from the pre-update replicas W^i
+        if (i > 0) {  // every CTA has stored W^i
+          for (int c = zt; c < (int)gridDim.x; c += nzt) flag_poll(fP2 + 32 * c, ep - 1u);
+          group_sync(2, nzt);
+        }
+        pmark(12);
+        // z^i of b2 (block 0's update): complete since round i - 1's ZD flags
+        if (blk == 0 && zt < classes) zb2s[zt] = ld_cg(zc + ob2 + zt);
+          const int64_t per = (a.n4 + gridDim.x - 1) / gridDim.x;
+          const int64_t c_lo = (int64_t)blockIdx.x * per;
+          const int64_t c_hi = c_lo + per < a.n4 ? c_lo + per : a.n4;
+          // two columns per thread and iteration, every load of a replica group issued
+          // before its arithmetic (the compiler cannot hoist loads across the stores)
+          const float4 zero = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int64_t c4 = c_lo + zt; c4 < c_hi; c4 += 2 * nzt) {
+            const bool two = c4 + nzt < c_hi;
+            const int64_t p0 = c4 << 2, p1 = (c4 + nzt) << 2;
+            const float4 z0 = ld_z4(zc + p0), zp0 = ld_z4(zo + p0);
+            const float4 z1 = two ? ld_z4(zc + p1) : zero;
+            const float4 zp1 = two ? ld_z4(zo + p1) : zero;
+            float4 s0 = zero, s1 = zero;
+            for (int jj = 0; jj < a.r; jj += 4) {
+              float4 w0[4], w1[4];
+    #pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                w0[u] = jj + u < a.r ? ld_z4(a.W + (int64_t)(jj + u) * a.ld + p0) : zero;
+                w1[u] = two && jj + u < a.r ? ld_z4(a.W + (int64_t)(jj + u) * a.ld + p1) : zero;
+              }
+    #pragma unroll
+              for (int u = 0; u < 4; ++u) {  // corrections added in ascending j
+                if (jj + u < a.r) {
+                  s0.x = __fadd_rn(s0.x, __fmul_rn(a.alpha, __fsub_rn(w0[u].x, z0.x)));
+                  s0.y = __fadd_rn(s0.y, __fmul_rn(a.alpha, __fsub_rn(w0[u].y, z0.y)));
+                  s0.z = __fadd_rn(s0.z, __fmul_rn(a.alpha, __fsub_rn(w0[u].z, z0.z)));
+                  s0.w = __fadd_rn(s0.w, __fmul_rn(a.alpha, __fsub_rn(w0[u].w, z0.w)));
+                  s1.x = __fadd_rn(s1.x, __fmul_rn(a.alpha, __fsub_rn(w1[u].x, z1.x)));
+                  s1.y = __fadd_rn(s1.y, __fmul_rn(a.alpha, __fsub_rn(w1[u].y, z1.y)));
+                  s1.z = __fadd_rn(s1.z, __fmul_rn(a.alpha, __fsub_rn(w1[u].z, z1.z)));
+                  s1.w = __fadd_rn(s1.w, __fmul_rn(a.alpha, __fsub_rn(w1[u].w, z1.w)));
+                }
+              }
+            }
+            float4 zn;
+            zn.x = __fadd_rn(__fadd_rn(z0.x, s0.x), __fmul_rn(a.mu, __fsub_rn(z0.x, zp0.x)));
+            zn.y = __fadd_rn(__fadd_rn(z0.y, s0.y), __fmul_rn(a.mu, __fsub_rn(z0.y, zp0.y)));
+            zn.z = __fadd_rn(__fadd_rn(z0.z, s0.z), __fmul_rn(a.mu, __fsub_rn(z0.z, zp0.z)));
+            zn.w = __fadd_rn(__fadd_rn(z0.w, s0.w), __fmul_rn(a.mu, __fsub_rn(z0.w, zp0.w)));
+            *reinterpret_cast<float4*>(zo + p0) = zn;
+            bad |= !finite4(zn);
+            if (two) {
+              zn.x = __fadd_rn(__fadd_rn(z1.x, s1.x), __fmul_rn(a.mu, __fsub_rn(z1.x, zp1.x)));
+              zn.y = __fadd_rn(__fadd_rn(z1.y, s1.y), __fmul_rn(a.mu, __fsub_rn(z1.y, zp1.y)));
+              zn.z = __fadd_rn(__fadd_rn(z1.z, s1.z), __fmul_rn(a.mu, __fsub_rn(z1.z, zp1.z)));
+              zn.w = __fadd_rn(__fadd_rn(z1.w, s1.w), __fmul_rn(a.mu, __fsub_rn(z1.w, zp1.w)));
+              *reinterpret_cast<float4*>(zo + p1) = zn;
+              bad |= !finite4(zn);
+            }
+          }
+          pmark(13);
+        group_sync(2, nzt);
+        if (zt == 0) st_release_gpu(fZD + 32 * blockIdx.x, ep);  // done reading W^i, z^{i+1} written
+        // every CTA has read W^i (before any replica store) and z^{i+1} is complete
+        for (int c = zt; c < (int)gridDim.x; c += nzt) flag_poll(fZD + 32 * c, ep);
+        group_sync(2, nzt);
+        pmark(14);
+        if (i + 1 < m.count && zw == 0) {  // prefetch round i + 1's z block
+          fence_proxy_async();  // z^{i+1} was written by other CTAs (generic proxy)
+          issue_z_warp(zo, (i + 1) & 1);
+        }
       }
       if (pre) {  // the next round's norms
         bulk::wait(&mbar[(i + 1) & 1], ((i + 1) >> 1) & 1);
@@ -575,7 +688,9 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
       group_sync(1, nt1);
       // b2^i: block 0 of learner j stored it in m.B2[i & 1][j] in round i - 1,
       // before its partial-logit flag of round i
-      if (i > 0 && tid < classes) b2s[tid] = ld_cg(m.B2 + ((i & 1) * m.a.r + j) * 32 + tid);
+      // (cluster mode: block 0 keeps its own b2 in b2s, which its peers read through DSMEM)
+      if (i > 0 && tid < classes && !(m.cl && blk == 0))
+        b2s[tid] = ld_cg(m.B2 + ((i & 1) * m.a.r + j) * 32 + tid);
       pmark(4);
       if (tid == 0) {
         fence_proxy_async();
@@ -587,13 +702,31 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
       if (i > 0) group_sync(1, nt1);  // b2s
       for (int q = tid; q < b * classes; q += nt1) {
         const int t = q / classes, c = q - t * classes;
-        float s = 0.f;
-        for (int k = 0; k < nblk; ++k) s = __fadd_rn(s, plg[k * npl + q]);  // ascending block
+        // four interleaved partial sums (blocks k = 0, 1, 2, 3 mod 4, each in
+        // ascending order), combined as ((s0 + s1) + (s2 + s3)): a fixed order
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        int k = 0;
+        for (; k + 4 <= nblk; k += 4) {
+          s0 = __fadd_rn(s0, plg[k * npl + q]);
+          s1 = __fadd_rn(s1, plg[(k + 1) * npl + q]);
+          s2 = __fadd_rn(s2, plg[(k + 2) * npl + q]);
+          s3 = __fadd_rn(s3, plg[(k + 3) * npl + q]);
+        }
+        for (; k < nblk; ++k) s0 = __fadd_rn(s0, plg[k * npl + q]);
+        const float s = __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));
         lg[t * 32 + c] = __fadd_rn(s, b2s[c]);
       }
       group_sync(1, nt1);
       pmark(5);
-      for (int t = warp; t < b; t += nw1) warp_softmax_grad(lg + t * 32, classes, yr[t], es + t * 32);
+      if (classes <= 16) {  // two rows per warp (half-warps), bitwise the same
+        for (int t = 2 * warp; t < b; t += 2 * nw1) {
+          const bool v1 = t + 1 < b;
+          halfwarp_softmax_grad(lg + t * 32, lg + (t + 1) * 32, classes, yr[t], v1 ? yr[t + 1] : 0, v1,
+                                es + t * 32, es + (t + 1) * 32);
+        }
+      } else {
+        for (int t = warp; t < b; t += nw1) warp_softmax_grad(lg + t * 32, classes, yr[t], es + t * 32);
+      }
       group_sync(1, nt1);
       pmark(6);
       for (int q = tid; q < kRows * U; q += nt1) {  // da1 = (W2^T e) [a1 > 0]  (W2^i)
@@ -603,10 +736,16 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
           for (int c = 0; c < classes; ++c) s = __fmaf_rn(w2s[c * U + ul], es[t * 32 + c], s);
         das[q] = msk[q] ? s : 0.f;
       }
+      if (UPDATE && m.cl) {  // the cluster barriers every thread takes part in
+        if (i > 0) cluster_wait();  // (P_{i-1})
+        cluster_arrive();           // (Z_i)
+      }
       pmark(7);
     }
     __syncthreads();  // join: das; (UPDATE) every CTA's z slice done; next rows staged
-    if (UPDATE) bulk::wait(&mbar[3 + (i & 1)], (i >> 1) & 1);  // this round's z^i block
+    if (UPDATE && m.cl) cluster_wait();  // (Z_i) the cluster's z^{i+1} parts stored, W^i read
+    // this round's z^i block (cluster mode: through DSMEM after round 0)
+    if (UPDATE && !(m.cl && i > 0)) bulk::wait(&mbar[3 + (i & 1)], (i >> 1) & 1);
     pmark(8);
 
     // ---- phase 2 (all warps): gradients of the block and the replica update.
@@ -654,6 +793,7 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
             const float wv = elem_w(b2s[c], g, zb2s[c], a.alpha, a.gamma, cc);
             W[ob2 + c] = wv;
             m.B2[(((i + 1) & 1) * m.a.r + j) * 32 + c] = wv;  // b2^{i+1} for the learner's CTAs
+            if (m.cl) b2s[c] = wv;  // (after every read of b2^i in this CTA: logits, da1's join)
             bad |= !isfinite(wv);
           }
         }
@@ -723,20 +863,26 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
     }
     pmark(10);
     // W^{i+1} of this block is stored (the next round's z slices read it)
-    if (UPDATE && i + 1 < m.count) flag_arrive(fP2 + 32 * blockIdx.x, ep);
-    else __syncthreads();  // shared buffers are reused by the next round
+    if (UPDATE && i + 1 < m.count && m.cl) {
+      __syncthreads();   // shared buffers are reused by the next round
+      cluster_arrive();  // (P_i) my W^{i+1} (shared memory) is complete for the peers
+    } else if (UPDATE && i + 1 < m.count) {
+      flag_arrive(fP2 + 32 * blockIdx.x, ep);
+    } else {
+      __syncthreads();  // shared buffers are reused by the next round
+    }
     pmark(11);
   }
   if (UPDATE && a.nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(a.nonfinite, 1);
   if (PROF && (tid == 0 || tid == nt1))
     for (int q = 0; q < 16; ++q)
-      if ((tid == 0) == (q < 12)) m.prof[blockIdx.x * 16 + q] = pacc[PROF ? q : 0];
+      if ((tid == 0) == (q < 12)) m.prof[blockIdx.x * 16 + q] = pacc[q];
 }
 
 size_t round_smem(int in_dim, int U, int CU, int nblk, int classes, int nx, int nzb) {
   const size_t xld = (size_t)in_dim + 4;
   const size_t fl = (size_t)nx * kRows * xld + (size_t)CU * xld + (size_t)nzb * U * xld +
-                    (size_t)kWarps * kRows * CU + 2 * (size_t)kRows * U + 2 * (size_t)kRows * 32 +
+                    (size_t)kSlices * kRows * CU + 2 * (size_t)kRows * U + 2 * (size_t)kRows * 32 +
                     2 * kRows + CU + 32 * (size_t)U + U + 2 * (32 * (size_t)U + U) +
                     (size_t)nblk * kRows * classes;
   return sizeof(float) * fl + (size_t)kRows * U + 16;
@@ -759,13 +905,13 @@ bool mlp_coop() {
 // Warps of group 2 (see the kernel): measured best 2 for one round per launch
 // and 4 for several (MLP rounds/s, b = 16, profiles/r02_mlp_fused.txt);
 // SMA_MLP_ZWARPS = 0 / 2 / 4 forces it.
-int mlp_zwarps(int count) {
+int mlp_zwarps(int count, bool cl = false) {
   static const int forced = [] {
     const char* e = getenv("SMA_MLP_ZWARPS");
     const int v = e ? atoi(e) : -1;
     return (v == 0 || v == 2 || v == 4) ? v : -1;
   }();
-  return forced >= 0 ? forced : (count > 1 ? 4 : 2);
+  return forced >= 0 ? forced : (count > 1 && !cl ? 4 : 2);
 }
 
 template <int TU, bool UPDATE>
@@ -782,8 +928,27 @@ cudaError_t launch_tu(const MlpRoundArgs& m, int grid, size_t smem, cudaStream_t
   cfg.blockDim = dim3(kThr);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[2];
+  cudaLaunchAttribute at[3];
   int n = 0;
+  if (m.cl) {  // the r CTAs of a unit block as one cluster (blockIdx.x = blk * r + j)
+    if (m.a.r > 8) {
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    at[n].id = cudaLaunchAttributeClusterDimension;
+    at[n].val.clusterDim.x = (unsigned)m.a.r;
+    at[n].val.clusterDim.y = 1;
+    at[n].val.clusterDim.z = 1;
+    ++n;
+    // every cluster must be resident at once (the CTAs wait on each other)
+    cfg.attrs = at;
+    cfg.numAttrs = n;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, k, &cfg) != cudaSuccess || nc * m.a.r < grid) {
+      cudaGetLastError();
+      return cudaErrorNotSupported;
+    }
+  }
   if (mlp_coop()) {
     at[n].id = cudaLaunchAttributeCooperative;
     at[n].val.cooperative = 1;
@@ -850,25 +1015,53 @@ cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* pe
   const int nblk = hidden / U;
   if (count > 1 && CU != U) return cudaErrorNotSupported;
   constexpr size_t kSmemMax = 225 * 1024;
+  // Cluster mode (SMA_MLP_CLUSTER=1, read per launch; off by default): the r CTAs
+  // of a unit block form a cluster and exchange z through DSMEM (no z slice,
+  // no ZD / P2 flags, no z TMA after round 0); needs r a power of two <= 16 and
+  // z^i and z^{i-1} of the block on chip (k <= 4 at the MLP shape).  Measured
+  // slower than the flag protocol (profiles/r02_mlp_fused.txt: k = 4 70.2k vs
+  // 77.2k rounds/s -- each cluster-scope release after the replica stores costs
+  // ~1.3 us, and the DSMEM z parts on 2 warps lengthen group 2), kept as a
+  // tested alternative (bitwise equal to the default).
+  const char* cl_env = getenv("SMA_MLP_CLUSTER");
+  const bool cl_knob = cl_env && cl_env[0] == '1';
+  const bool cl_ok = cl_knob && update && CU == U && a.r >= 2 && a.r <= 16 && (a.r & (a.r - 1)) == 0 &&
+                     mlp_zwarps(count) > 0;
   int nx = 1, nzb = 0;
-  if (count > 1) {
-    const int cand[3][2] = {{2, 2}, {2, 0}, {1, 0}};
-    int q = 0;
-    while (q < 3 && round_smem(in_dim, U, CU, nblk, classes, cand[q][0], cand[q][1]) > kSmemMax) ++q;
-    if (q == 3) return cudaErrorNotSupported;
-    nx = cand[q][0];
-    nzb = cand[q][1];
-  } else {
-    if (round_smem(in_dim, U, CU, nblk, classes, 1, 0) > kSmemMax) return cudaErrorNotSupported;
+  auto configure = [&](bool cl) -> bool {
+    nx = 1;
+    nzb = 0;
+    if (count > 1) {
+      const int cand_fl[3][2] = {{2, 2}, {2, 0}, {1, 0}};
+      const int cand_cl[2][2] = {{2, 2}, {1, 2}};  // z^i and z^{i-1} of the block on chip
+      const int nc = cl ? 2 : 3;
+      for (int q = 0; q < nc; ++q) {
+        const int* c = cl ? cand_cl[q] : cand_fl[q];
+        if (round_smem(in_dim, U, CU, nblk, classes, c[0], c[1]) <= kSmemMax) {
+          nx = c[0];
+          nzb = c[1];
+          return true;
+        }
+      }
+      return false;
+    }
+    if (cl) {
+      nzb = 2;
+      return round_smem(in_dim, U, CU, nblk, classes, 1, 2) <= kSmemMax;
+    }
+    if (round_smem(in_dim, U, CU, nblk, classes, 1, 0) > kSmemMax) return false;
     if (update && CU == U && round_smem(in_dim, U, CU, nblk, classes, 1, 1) <= kSmemMax) nzb = 1;
-  }
-  const size_t smem = round_smem(in_dim, U, CU, nblk, classes, nx, nzb);
+    return true;
+  };
+  bool cl = cl_ok && configure(true);
+  if (!cl && !configure(false)) return cudaErrorNotSupported;
+  size_t smem = round_smem(in_dim, U, CU, nblk, classes, nx, nzb);
   MlpRoundArgs m{};
   m.X = X; m.y = y; m.perm = perm; m.pos0 = pos0;
   m.b = b; m.in_dim = in_dim; m.hidden = hidden; m.classes = classes; m.j0 = j0;
   m.kb = kb; m.count = count;
-  m.nzw = mlp_zwarps(count);
-  m.U = U; m.nblk = nblk; m.nch = U / CU; m.nx = nx; m.nzb = nzb;
+  m.nzw = mlp_zwarps(count, cl);
+  m.U = U; m.nblk = nblk; m.nch = U / CU; m.nx = nx; m.nzb = nzb; m.cl = cl ? 1 : 0;
   m.PL = PL; m.B2 = PL + 2 * (size_t)num_sms * kRows * 32; m.G = G; m.bar = bar; m.a = a;
   m.fstride = num_sms; m.epoch = epoch;
   m.prof = mlp_prof_buffer();
@@ -877,11 +1070,20 @@ cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* pe
 #define SMA_MLP_ROUND(TU)                                                                      \
   e = update ? launch_tu<TU, true>(m, grid, smem, s) : launch_tu<TU, false>(m, grid, smem, s); \
   break;
-  switch (CU / kUG) {
-    case 1: SMA_MLP_ROUND(1)
-    case 2: SMA_MLP_ROUND(2)
-    case 4: SMA_MLP_ROUND(4)
-    default: SMA_MLP_ROUND(8)
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    switch (CU / kUG) {
+      case 1: SMA_MLP_ROUND(1)
+      case 2: SMA_MLP_ROUND(2)
+      case 4: SMA_MLP_ROUND(4)
+      default: SMA_MLP_ROUND(8)
+    }
+    // the clusters cannot all be resident: the flag-only configuration
+    if (e != cudaErrorNotSupported || !m.cl || !configure(false)) break;
+    m.cl = 0;
+    m.nx = nx;
+    m.nzb = nzb;
+    m.nzw = mlp_zwarps(count, false);
+    smem = round_smem(in_dim, U, CU, nblk, classes, nx, nzb);
   }
 #undef SMA_MLP_ROUND
   static int launches = 0;
@@ -891,13 +1093,13 @@ cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* pe
     cudaMemcpy(t.data(), m.prof, t.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
     int clk_khz = 0;
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
-    const char* names[] = {"loop", "rows+norms", "phase1", "PL_flag", "join(zslice)", "PL_wait",
-                           "logits", "softmax", "da1+ZD_wait+z", "dW2/db", "dW1+update", "P2_flag",
-                           "z:P2_wait", "z:slice", "z:ZD_flag"};
-    fprintf(stderr, "SMA_MLP_PROF launch %d (r=%d U=%d CU=%d nx=%d nzb=%d count=%d grid=%d "
-            "smem=%zu) us per round at %.0f MHz, mean / max over CTAs:", launches, a.r, U, CU, nx,
-            nzb, count, grid, smem, clk_khz * 1e-3);
-    for (int q = 0; q < 15; ++q) {
+    const char* names[] = {"loop", "rows(nx=1)", "phase1", "PL_flag", "PL_wait", "logits",
+                           "softmax", "da1", "join+z_wait", "dW2/db", "dW1+update", "P2_flag",
+                           "g2:rows+P2_wait", "g2:z_slice", "g2:ZD_flag+wait", "g2:prefetch+norms"};
+    fprintf(stderr, "SMA_MLP_PROF launch %d (cluster=%d r=%d U=%d CU=%d nx=%d nzb=%d count=%d grid=%d "
+            "smem=%zu) us per round at %.0f MHz, mean / max over CTAs:", launches, m.cl, a.r, U, CU,
+            m.nx, m.nzb, count, grid, smem, clk_khz * 1e-3);
+    for (int q = 0; q < 16; ++q) {
       double sum = 0, mx = 0;
       for (int c = 0; c < grid; ++c) {
         const double v = (double)t[(size_t)c * 16 + q];

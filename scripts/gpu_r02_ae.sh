@@ -1,0 +1,10 @@
+# round 2, call AE: cluster mode opt-in (SMA_MLP_CLUSTER=1, read per launch) -- MLP tests incl. cluster == flag
+# protocol bitwise; default benches
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+S=gpurun_out/status_ae.txt; : > $S
+timeout 1500 python -m pytest -q -x -rfs -k "mlp or learner" tests/test_gpu_parity.py > gpurun_out/ae_pytest.log 2>&1; echo pytest=$? >> $S
+for k in 4 8 16 32; do
+  timeout 300 python bench.py --config MLP --k $k --steps 3000 --warmup 50 --rounds-per-call 3000 --no-cpu-baseline --no-e2e > gpurun_out/ae_multi_k$k.log 2>&1
+  timeout 300 python bench.py --config MLP --k $k --steps 3000 --warmup 50 --no-cpu-baseline --no-e2e > gpurun_out/ae_one_k$k.log 2>&1
+done
+echo done >> $S

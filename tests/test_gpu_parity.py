@@ -755,6 +755,42 @@ def test_mlp_learner_steps_multi_round_bitwise(torch_cuda, S, orc, k):
         h.close()
 
 
+def test_mlp_cluster_mode_bitwise(torch_cuda, S, orc):
+    """The fused MLP kernel's cluster mode (SMA_MLP_CLUSTER=1: the 4 CTAs of a
+    unit block form a thread-block cluster and exchange z^{i+1} through
+    distributed shared memory instead of the z slice and the ZD / P2 flag lines)
+    is bitwise equal to the default flag protocol, one round per launch and
+    several, over 30 epoch-crossing rounds at k = 4."""
+    import os
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(2_000, seed=21)
+    k, b, R = 4, 16, 30
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    w0 = np.random.default_rng(6).normal(0, 0.05, MLP_D).astype(np.float32)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    out = []
+    for cl, multi in (("0", True), ("1", True), ("1", False)):
+        os.environ["SMA_MLP_CLUSTER"] = cl   # read per launch
+        try:
+            h = S.Sma(MLP_D, k, a, g, m, w0)
+            S.sma_learner_attach(h.h, 1, 784, 256, 10, b, Xd, yd, X.shape[0], 7)
+            s = torch.cuda.Stream()
+            if multi:
+                S.sma_learner_steps(h.h, 0, R, s)
+            else:
+                for i in range(R):
+                    S.sma_learner_step(h.h, i, s)
+            s.synchronize()
+            out.append((h.central(), h.central_prev(), [h.replica(j) for j in range(k)]))
+            h.close()
+        finally:
+            os.environ.pop("SMA_MLP_CLUSTER", None)
+    for z, zp, W in out[1:]:
+        assert np.array_equal(z, out[0][0]) and np.array_equal(zp, out[0][1])
+        for j in range(k):
+            assert np.array_equal(W[j], out[0][2][j]), j
+
+
 def test_learner_steps_softmax_is_per_round(torch_cuda, S, orc):
     """sma_learner_steps on the softmax learner (no multi-round kernel) equals
     sma_learner_step per round bitwise, and the oracle within the bar (C1)."""
