@@ -35,6 +35,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "sma_bulk.cuh"
@@ -122,6 +123,7 @@ struct MlpRoundArgs {
   int nx;                 // batch-row buffers: 2 = the next round's rows prefetched
   int nzb;                // z-row buffers of the W1 block: 0 (z read from L2), 1, or 2 (prefetched)
   int nzw;                // UPDATE: warps of group 2 (0 = it runs on all warps, after phase 1)
+  int bexp;               // certainty threshold 2^bexp (R18; >= 6x the dot's error bound)
   int cl;                 // UPDATE, cluster mode: the r CTAs of one unit block form a thread-block
                           // cluster (blockIdx.x = blk * r + j) and exchange z through it
   float* PL;              // [2][grid][kRows][classes] partial logits (round parity)
@@ -437,8 +439,13 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
           for (int w = 0; w < kSlices; ++w) s = __fadd_rn(s, part[(w * kRows + t) * CU + ul]);
           const float bias = b1s[uc + ul];
           const float av = __fadd_rn(s, bias);
-          // |fl(a) - a| <= ~110 u (sum |w x| + |b|) << 2^-12 (||w|| ||x|| + |b|)
-          const float bound = ldexpf(__fmaf_rn(wn[ul], xnr[t], fabsf(bias)), -12);
+          // fl(a) sums at most n = 4 ceil(in_dim / (4 kSlices)) + kSlices + 1 terms
+          // along any path (a slice's FMA chain, the slice partials, the bias), so
+          // |fl(a) - a| <= gamma_n (sum |w x| + |b|) <= gamma_n (||w|| ||x|| + |b|)
+          // (Cauchy-Schwarz); the launcher's threshold 2^bexp >= 6 gamma_n keeps a
+          // 6x margin over it and over the norms' own rounding (in_dim = 784:
+          // n = 81, 2^-15; round 1's 2^-12 sent ~8x more entries to the Dot2).
+          const float bound = ldexpf(__fmaf_rn(wn[ul], xnr[t], fabsf(bias)), m.bexp);
           const int o = t * U + uc + ul;
           if (t < b && fabsf(av) <= bound) {
             const int slot = atomicAdd(&n_unc, 1);
@@ -1060,6 +1067,11 @@ cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* pe
   m.X = X; m.y = y; m.perm = perm; m.pos0 = pos0;
   m.b = b; m.in_dim = in_dim; m.hidden = hidden; m.classes = classes; m.j0 = j0;
   m.kb = kb; m.count = count;
+  {  // R18 threshold: 2^bexp >= 6 gamma_n, n = the longest summation path of a1
+    const int n = 4 * ((in_dim / 4 + kSlices - 1) / kSlices) + kSlices + 1;
+    m.bexp = (int)std::ceil(std::log2(6.0 * n * std::ldexp(1.0, -24) * (1.0 + 1e-6)));
+    if (m.bexp < -15) m.bexp = -15;
+  }
   m.nzw = mlp_zwarps(count, cl);
   m.U = U; m.nblk = nblk; m.nch = U / CU; m.nx = nx; m.nzb = nzb; m.cl = cl ? 1 : 0;
   m.PL = PL; m.B2 = PL + 2 * (size_t)num_sms * kRows * 32; m.G = G; m.bar = bar; m.a = a;
