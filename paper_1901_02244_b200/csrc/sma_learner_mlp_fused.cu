@@ -124,6 +124,7 @@ struct MlpRoundArgs {
   int nzb;                // z-row buffers of the W1 block: 0 (z read from L2), 1, or 2 (prefetched)
   int nzw;                // UPDATE: warps of group 2 (0 = it runs on all warps, after phase 1)
   int bexp;               // certainty threshold 2^bexp (R18; >= 6x the dot's error bound)
+  float bscale;           // 2^bexp
   int cl;                 // UPDATE, cluster mode: the r CTAs of one unit block form a thread-block
                           // cluster (blockIdx.x = blk * r + j) and exchange z through it
   float* PL;              // [2][grid][kRows][classes] partial logits (round parity)
@@ -382,8 +383,12 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
         // depend on the group sizes, so one round per launch (2 group-2 warps)
         // and several (4) give the same bits
         for (int sl = warp; sl < kSlices; sl += nw1) {
-          const int rg = lane >> 2, ug = lane & 3;  // 8 row groups x 4 unit groups
-          const int t0 = rg * kTR;
+          // 8 row groups x 4 unit groups; row group rg takes batch rows rg and
+          // rg + 8: with the 788-float row stride (197 float4 = 5 mod 8 bank
+          // groups) the 8 rows of one 128-bit load land on 8 distinct bank groups
+          // (rows 2rg, 2rg + 1 had 2-way conflicts)
+          const int rg = lane >> 2, ug = lane & 3;
+          const int t0 = rg;
           const int n4k = in_dim >> 2;
           const int k4a = sl * n4k / kSlices, k4b = (sl + 1) * n4k / kSlices;
           float acc[kTR][TU];
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
             for (int q = 0; q < kTR; ++q) acc[q][u] = 0.f;
           }
           const float4* xr0 = reinterpret_cast<const float4*>(xr + t0 * xld);
-          const float4* xr1 = reinterpret_cast<const float4*>(xr + (t0 + 1) * xld);
+          const float4* xr1 = reinterpret_cast<const float4*>(xr + (t0 + kRows / kTR) * xld);
   #pragma unroll 2
           for (int k4 = k4a; k4 < k4b; ++k4) {
             float4 wv[TU];
@@ -416,7 +421,7 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
           for (int u = 0; u < TU; ++u) {
             const int ul = ug + kUG * u;
   #pragma unroll
-            for (int q = 0; q < kTR; ++q) part[(sl * kRows + t0 + q) * CU + ul] = acc[q][u];
+            for (int q = 0; q < kTR; ++q) part[(sl * kRows + t0 + q * (kRows / kTR)) * CU + ul] = acc[q][u];
           }
         }
         for (int ul = warp; ul < CU; ul += nw1) {  // ||W1[u]|| (one warp per unit, fixed order)
@@ -445,7 +450,7 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
           // (Cauchy-Schwarz); the launcher's threshold 2^bexp >= 6 gamma_n keeps a
           // 6x margin over it and over the norms' own rounding (in_dim = 784:
           // n = 81, 2^-15; round 1's 2^-12 sent ~8x more entries to the Dot2).
-          const float bound = ldexpf(__fmaf_rn(wn[ul], xnr[t], fabsf(bias)), m.bexp);
+          const float bound = __fmul_rn(__fmaf_rn(wn[ul], xnr[t], fabsf(bias)), m.bscale);  // exact: 2^bexp
           const int o = t * U + uc + ul;
           if (t < b && fabsf(av) <= bound) {
             const int slot = atomicAdd(&n_unc, 1);
@@ -1006,9 +1011,14 @@ cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* pe
     return cudaErrorNotSupported;
   // the fewest units per CTA (4, 8, ..., 64) whose grid r * hidden / U fits one
   // CTA per SM, with U dividing hidden
+  // (SMA_MLP_U = 4 ... 64, experiments: a larger U on fewer CTAs)
+  static const int u_knob = [] {
+    const char* e = getenv("SMA_MLP_U");
+    return e ? atoi(e) : 0;
+  }();
   int U = 0;
   for (int u = 4; u <= 64; u *= 2)
-    if (hidden % u == 0 && (int64_t)a.r * (hidden / u) <= num_sms) {
+    if (hidden % u == 0 && (int64_t)a.r * (hidden / u) <= num_sms && u >= u_knob) {
       U = u;
       break;
     }
@@ -1071,6 +1081,7 @@ cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* pe
     const int n = 4 * ((in_dim / 4 + kSlices - 1) / kSlices) + kSlices + 1;
     m.bexp = (int)std::ceil(std::log2(6.0 * n * std::ldexp(1.0, -24) * (1.0 + 1e-6)));
     if (m.bexp < -15) m.bexp = -15;
+    m.bscale = std::ldexp(1.0f, m.bexp);
   }
   m.nzw = mlp_zwarps(count, cl);
   m.U = U; m.nblk = nblk; m.nch = U / CU; m.nx = nx; m.nzb = nzb; m.cl = cl ? 1 : 0;
