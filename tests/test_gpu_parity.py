@@ -755,6 +755,73 @@ def test_mlp_learner_steps_multi_round_bitwise(torch_cuda, S, orc, k):
         h.close()
 
 
+# (in_dim, hidden, classes, b, k): the fused kernel's shape space -- units per CTA
+# U from 4 to 64 (phase-1 chunks CU < U at U = 64), ragged and power-of-two
+# batches (the fdiv and the exact-multiply paths), classes > 16 (the full-warp
+# softmax), odd learner counts; in_dim % 4 == 0 (the kernel's requirement)
+MLP_SHAPES = [(64, 32, 3, 5, 3), (128, 64, 17, 16, 4), (96, 128, 10, 7, 2), (784, 256, 10, 9, 5),
+              (256, 512, 24, 16, 6), (40, 96, 6, 12, 3)]
+
+
+@pytest.mark.parametrize("shape", MLP_SHAPES, ids=[str(x) for x in MLP_SHAPES])
+def test_mlp_fused_shapes_per_round(torch_cuda, S, orc, shape):
+    """The fused MLP kernel over a spread of learner shapes: 12 rounds, one launch
+    per round, each checked against the fp64 oracle from the GPU's state before
+    it, as in test_mlp_bench_configs_per_round_100_rounds (state <= 1e-6,
+    recovered gradients within 2e-6 plus the fp32 rounding of the update); then
+    the same 12 rounds as one multi-round launch, bitwise equal."""
+    torch = torch_cuda
+    in_dim, hidden, classes, b, k = shape
+    D = hidden * in_dim + hidden + classes * hidden + classes
+    X, y = sma_inputs.blobs(max(600, 3 * k * b), dim=in_dim, classes=classes, seed=in_dim + hidden)
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    w0 = np.random.default_rng(hidden).normal(0, 0.1, D).astype(np.float32)
+    h = S.Sma(D, k, a, g, m, w0)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    seed = 5
+    S.sma_learner_attach(h.h, 1, in_dim, hidden, classes, b, Xd, yd, X.shape[0], seed)
+    s = torch.cuda.Stream()
+    worst = dict(state=0.0, grad=0.0)
+
+    def check_round(i, Wg, z, zp, after):
+        st = orc.State(Wg, z, zp)
+        G = np.stack([orc.mlp_loss_grad(X, y, orc.batch_indices(X.shape[0], k, b, seed, i, j), Wg[j],
+                                        in_dim, hidden, classes)[1] for j in range(k)])
+        z_before = st.z.copy()
+        st.round(G, a, g, m)
+        zn, zpn, Wn = after
+        worst["state"] = max(worst["state"], relerr(zn, st.z), relerr(zpn, st.z_prev))
+        for j in range(k):
+            worst["state"] = max(worst["state"], relerr(Wn[j], st.W[j]))
+            c = a * (Wg[j] - z_before)
+            gg = (Wg[j] - c - Wn[j].astype(np.float64)) / g
+            tol = 2e-6 + 2.0 ** -21 * (np.abs(Wg[j]) + np.abs(Wn[j])) / g
+            worst["grad"] = max(worst["grad"], float(np.max(np.abs(gg - G[j]) / tol)))
+        assert worst["state"] <= 1e-6 and worst["grad"] <= 1.0, (i, worst)
+
+    def state():
+        s.synchronize()
+        return (h.central().astype(np.float64), h.central_prev().astype(np.float64),
+                np.stack([h.replica(j) for j in range(k)]).astype(np.float64))
+
+    for i in range(12):   # one launch per round, every round vs the oracle
+        z, zp, Wg = state()
+        S.sma_learner_step(h.h, i, s)
+        check_round(i, Wg, z, zp, state())
+    # the same 12 rounds as ONE multi-round launch on a second handle: bitwise equal
+    h2 = S.Sma(D, k, a, g, m, w0)
+    S.sma_learner_attach(h2.h, 1, in_dim, hidden, classes, b, Xd, yd, X.shape[0], seed)
+    S.sma_learner_steps(h2.h, 0, 12, s)
+    s.synchronize()
+    assert np.array_equal(h.central(), h2.central())
+    assert np.array_equal(h.central_prev(), h2.central_prev())
+    for j in range(k):
+        assert np.array_equal(h.replica(j), h2.replica(j)), j
+    print("MLP-SHAPE", dict(shape=shape, **worst))
+    h.close()
+    h2.close()
+
+
 def test_mlp_cluster_mode_bitwise(torch_cuda, S, orc):
     """The fused MLP kernel's cluster mode (SMA_MLP_CLUSTER=1: the 4 CTAs of a
     unit block form a thread-block cluster and exchange z^{i+1} through
