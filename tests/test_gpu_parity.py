@@ -822,6 +822,45 @@ def test_mlp_fused_shapes_per_round(torch_cuda, S, orc, shape):
     h2.close()
 
 
+@pytest.mark.parametrize("k", [4, 16])
+def test_mlp_learner_steps_random_calls_stress(torch_cuda, S, orc, k):
+    """300 rounds through sma_learner_steps calls of random sizes (1-40 rounds,
+    seeded), back to back on one stream -- launches of the flag protocol
+    following each other under programmatic dependent launch, crossing epochs
+    (E = 31 / 7 rounds) -- bitwise equal to one sma_learner_step per round."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(2_000, seed=21)
+    b, R = 16, 300
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    w0 = np.random.default_rng(6).normal(0, 0.05, MLP_D).astype(np.float32)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    sizes = []
+    rng = np.random.default_rng(2024 + k)
+    while sum(sizes) < R:
+        sizes.append(int(min(rng.integers(1, 41), R - sum(sizes))))
+    hs = []
+    for multi in (False, True):
+        h = S.Sma(MLP_D, k, a, g, m, w0)
+        S.sma_learner_attach(h.h, 1, 784, 256, 10, b, Xd, yd, X.shape[0], 7)
+        s = torch.cuda.Stream()
+        if multi:
+            i = 0
+            for n in sizes:
+                S.sma_learner_steps(h.h, i, n, s)
+                i += n
+        else:
+            for i in range(R):
+                S.sma_learner_step(h.h, i, s)
+        s.synchronize()
+        hs.append(h)
+    assert np.array_equal(hs[0].central(), hs[1].central())
+    assert np.array_equal(hs[0].central_prev(), hs[1].central_prev())
+    for j in range(k):
+        assert np.array_equal(hs[0].replica(j), hs[1].replica(j)), j
+    for h in hs:
+        h.close()
+
+
 def test_mlp_cluster_mode_bitwise(torch_cuda, S, orc):
     """The fused MLP kernel's cluster mode (SMA_MLP_CLUSTER=1: the 4 CTAs of a
     unit block form a thread-block cluster and exchange z^{i+1} through
