@@ -809,7 +809,7 @@ def main():
                         "of dependent phases, latency-bound, not FLOP-bound",
                 "timing": timing_src if fused else "timed window / K (CUDA events on the launching "
                                                    "stream around the K rounds)"}
-        if not args.no_cpu_baseline and not learner:
+        if not args.no_cpu_baseline and not learner and world == 1:   # rank 0 at N = 1 only
             line["cpu_baseline"] = cpu_baseline(d, k, alpha, gamma, mu)
         print(json.dumps(line), flush=True)
     h.close()
