@@ -285,8 +285,8 @@ __global__ void __launch_bounds__(kThreads, kMinBlocks) replica_step_ldg(const R
 #define SMA_SPLIT_MINB 4
 #endif
 constexpr int kSplitMinBlocks = SMA_SPLIT_MINB;  // resident CTAs per SM the register budget allows
-template <int MODE, int G, int UJ = 2, int MINB = kSplitMinBlocks>
-__global__ void __launch_bounds__(kThreads, MINB) replica_step_split(const ReplicaArgs a) {
+template <int MODE, int G, int UJ = 2>
+__global__ void __launch_bounds__(kThreads, kSplitMinBlocks) replica_step_split(const ReplicaArgs a) {
   pdl::wait_and_release();
   constexpr int CPW = 32 / G;  // columns per warp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -828,19 +828,6 @@ cudaError_t launch_replica_step(int mode, bool tma, const ReplicaArgs& a0, int n
   else e = uj == 4 ? launch_pdl(replica_step_split<M, 2, 4>, grid, s, a)                      \
                    : launch_pdl(replica_step_split<M, 2>, grid, s, a);
     cudaError_t e = cudaSuccess;
-    // SMA_SPLIT_MINB_RT = 6|8 (experiments, fused mode, G = 2): a register budget
-    // for 6 / 8 resident CTAs per SM, so the C2 / C3 grid fits one wave
-    static const int minb_knob = [] {
-      const char* e = getenv("SMA_SPLIT_MINB_RT");
-      return e ? atoi(e) : 0;
-    }();
-    if (mode == kFused && G == 2 && (minb_knob == 6 || minb_knob == 8)) {
-      if (minb_knob == 6)
-        return uj == 4 ? launch_pdl(replica_step_split<kFused, 2, 4, 6>, grid, s, a)
-                       : launch_pdl(replica_step_split<kFused, 2, 2, 6>, grid, s, a);
-      return uj == 4 ? launch_pdl(replica_step_split<kFused, 2, 4, 8>, grid, s, a)
-                     : launch_pdl(replica_step_split<kFused, 2, 2, 8>, grid, s, a);
-    }
     switch (mode) {
       case kFused: SMA_SPLIT_LAUNCH(kFused) break;
       case kPartialA: SMA_SPLIT_LAUNCH(kPartialA) break;
