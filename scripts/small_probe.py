@@ -6,6 +6,7 @@ effective rate.  Measurement only (scripts/README.md)."""
 import json
 import os
 import sys
+import time
 
 import numpy as np
 import torch
@@ -28,18 +29,43 @@ for d, k in cases:
         h.step(s)
     s.synchronize()
     best = None
+    host_us = None
     for rep in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
+        t0 = time.perf_counter()
         for _ in range(steps):
             h.step(s)
+        th = (time.perf_counter() - t0) * 1e6 / steps   # host enqueue time per sma_step
         e1.record(s)
         e1.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / steps
-        best = us if best is None else min(best, us)
+        if best is None or us < best:
+            best, host_us = us, th
+    # the same rounds replayed from a CUDA graph of 100 captured sma_step calls
+    # (no host work between rounds): is the floor the host or the GPU?
+    graph_us = None
+    try:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            cs = torch.cuda.current_stream()
+            for _ in range(100):
+                h.step(cs)
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        cs = torch.cuda.current_stream()
+        e0.record(cs)
+        for _ in range(steps // 100):
+            g.replay()
+        e1.record(cs)
+        e1.synchronize()
+        graph_us = e0.elapsed_time(e1) * 1e3 / (100 * (steps // 100))
+    except Exception as ex:  # noqa: BLE001
+        graph_us = f"capture failed: {ex}"[:200]
     dp = h.d_pad
     b = 4 * dp * (3 * k + 3)
-    print(json.dumps({"d": d, "k": k, "d_pad": dp, "us_per_round": best, "bytes": b,
+    print(json.dumps({"d": d, "k": k, "d_pad": dp, "us_per_round": best, "host_enqueue_us": host_us, "graph100_us_per_round": graph_us, "bytes": b,
                       "eff_tbs": b / (best * 1e-6) / 1e12,
                       "env": {x: os.environ[x] for x in os.environ if x.startswith("SMA_")}}),
           flush=True)
