@@ -782,31 +782,41 @@ def main():
             line["config"]["rounds_per_call"] = args.rounds_per_call
             line["config"]["l2"] = ("L2-resident working set (replicas, gradients, z and the "
                                     "dataset's batch rows): not flushed")
-        if args.config == "MLP" and mode == "fused":
-            # the round is ONE cooperative kernel (learner gradient + fused update,
-            # sma_learner_mlp_fused.cu) unless SMA_MLP_FUSED=0 / SMA_MLP_TC force the
-            # five-kernel path: a FLOP roofline against the FP32 FFMA peak
+        if args.config in ("MLP", "C1") and mode == "fused":
+            # the round is ONE kernel (learner gradient + fused update:
+            # sma_learner_mlp_fused.cu, or the softmax cluster of
+            # sma_learner_softmax_fused.cu) unless disabled: a FLOP roofline
+            # against the FP32 FFMA peak
             bsz, hid, ind, ncls = cfg["batch"], 256, 784, 10
-            flops = r * (4 * bsz * ind * hid + 6 * bsz * hid * ncls)
+            if args.config == "MLP":
+                flops = r * (4 * bsz * ind * hid + 6 * bsz * hid * ncls)
+            else:   # logits + dW: r (2 b in_dim classes + 2 b in_dim classes)
+                flops = r * 4 * bsz * ind * ncls
             fused = launches == args.steps
             multi = args.rounds_per_call > 1 and launches < args.steps
             ms_k = kern_avg if fused else ms_max / args.steps
             mhz = clk.get("sm_mhz") or 1965.0
             peak_tf = 148 * 4 * 32 / 2 * 2 * mhz * 1e6 / 1e12
             ach = flops / (ms_k * 1e-3) / 1e12
+            kn = "mlp_round_kernel<TU, true>" if args.config == "MLP" else \
+                f"softmax_cluster_kernel (one {r}-CTA cluster: {r} of 148 SMs)"
             line["roofline"] = {
-                "bound": "alu", "kernel": "mlp_round_kernel<TU, true>" if fused else
-                (f"mlp_round_kernel<TU, true>, {launches} launches for {args.steps} rounds "
+                "bound": "alu", "kernel": kn if fused else
+                (f"{kn}, {launches} launches for {args.steps} rounds "
                  "(the rounds of one epoch per launch); per-round time = window / K" if multi else
-                 "5-kernel MLP learner + replica kernel (whole round)"),
+                 "per-round learner kernels + replica kernel (whole round)"),
                 "achieved": ach, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach / peak_tf,
                 "traffic": None, "flops_per_launch": flops, "avg_launch_ms": ms_k,
                 "peak_source": "derived: 148 SMs x 4 SMSPs x 32 lanes / FFMA reciprocal "
                                "throughput 2 (B300_MICROARCH.md: 3-register FFMA rt_SMSP = 2) x 2 "
                                f"FLOP x {mhz:.0f} MHz (median SM clock under load)",
-                "note": "FLOPs = r (4 b in_dim hidden + 6 b hidden classes): layer 1, dW1, "
-                        "logits, dW2, da1; the per-learner GEMMs are 16 x 784 x 256 -- a chain "
-                        "of dependent phases, latency-bound, not FLOP-bound",
+                "note": ("FLOPs = r (4 b in_dim hidden + 6 b hidden classes): layer 1, dW1, "
+                         "logits, dW2, da1; the per-learner GEMMs are 16 x 784 x 256 -- a chain "
+                         "of dependent phases, latency-bound, not FLOP-bound"
+                         if args.config == "MLP" else
+                         "FLOPs = r 4 b in_dim classes (logits, dW); one CTA per learner on "
+                         "r SMs -- a chain of dependent phases (logits, softmax, z exchange, "
+                         "dW, update) with two cluster barriers per round, latency-bound"),
                 "timing": timing_src if fused else "timed window / K (CUDA events on the launching "
                                                    "stream around the K rounds)"}
         if not args.no_cpu_baseline and not learner and world == 1:   # rank 0 at N = 1 only

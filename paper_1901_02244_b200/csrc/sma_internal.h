@@ -130,6 +130,17 @@ cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* pe
                              int64_t kb, int count, int b, int in_dim, int hidden, int classes,
                              int j0, float* PL, unsigned* bar, unsigned epoch, float* G,
                              const ReplicaArgs& a, bool update, int num_sms, cudaStream_t s);
+// The softmax-regression learner (kind 0) AND the n = 1 round for `count`
+// consecutive rounds of one epoch as ONE thread-block cluster of r CTAs
+// (sma_learner_softmax_fused.cu): replicas, z and batch rows on chip, z
+// exchanged through distributed shared memory; G receives the last round's
+// gradients.  cudaErrorNotSupported (nothing launched) outside its shapes or
+// when disabled (SMA_SOFTMAX_CLUSTER=0).
+bool softmax_cluster_enabled();
+cudaError_t launch_softmax_cluster_rounds(const float* X, const int32_t* y, const int32_t* perm,
+                                          int64_t pos0, int64_t kb, int count, int b, int in_dim,
+                                          int classes, int j0, float* G, const ReplicaArgs& a,
+                                          cudaStream_t s);
 // MLP layer 1 on tcgen05 (3xTF32 + |.| bound MMAs, cluster K-split); returns
 // cudaErrorNotSupported without launching when the shape is outside its path.
 cudaError_t launch_mlp_hidden_tc(const float* X, const int32_t* perm, int64_t pos0, int b,

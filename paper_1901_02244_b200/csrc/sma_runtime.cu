@@ -1370,14 +1370,17 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
   return mark_done(h, s);
 }
 
-// The n = 1 MLP round in the fused kernel (sma_learner_mlp_fused.cu) applies.
+// The n = 1 learner round in one fused kernel applies: the MLP kernel
+// (sma_learner_mlp_fused.cu) or the softmax cluster kernel
+// (sma_learner_softmax_fused.cu).
 static bool mlp_fused_ok(const sma_handle* h) {
-  return h->kind == 1 && !h->collective && !h->matc && h->r > 0 && !(h->graphs && !h->timing) &&
-         mlp_fused_enabled();
+  return !h->collective && !h->matc && h->r > 0 && !(h->graphs && !h->timing) &&
+         ((h->kind == 1 && mlp_fused_enabled()) || (h->kind == 0 && softmax_cluster_enabled()));
 }
 
 // Rounds [round0, round0 + count) of ONE epoch, with the learner in the loop,
-// in one launch of the fused MLP kernel.  *unsupported (nothing enqueued) when
+// in one launch of the fused learner kernel (MLP, or the softmax cluster).
+// *unsupported (nothing enqueued) when
 // the kernel does not cover the shape or count.
 static sma_status fused_mlp_rounds(sma_handle* h, int64_t round0, int count, cudaStream_t s,
                                    bool* unsupported) {
@@ -1407,9 +1410,13 @@ static sma_status fused_mlp_rounds(sma_handle* h, int64_t round0, int count, cud
   STATUS_TRY(timer_pair(h, SMA_PHASE_REPLICA, &tp));
   if (tp) CUDA_TRY(cudaEventRecord(tp[0], s));
   const cudaError_t e =
-      launch_mlp_round(h->X, h->y, h->perm_dev[buf], pos0, (int64_t)h->cfg.k * h->batch, count,
-                       h->batch, h->in_dim, h->hidden, h->classes, h->j0, h->mlp_PL, h->mlp_bar,
-                       h->mlp_epoch + 1, h->G, a, true, h->num_sms, s);
+      h->kind == 0
+          ? launch_softmax_cluster_rounds(h->X, h->y, h->perm_dev[buf], pos0,
+                                          (int64_t)h->cfg.k * h->batch, count, h->batch, h->in_dim,
+                                          h->classes, h->j0, h->G, a, s)
+          : launch_mlp_round(h->X, h->y, h->perm_dev[buf], pos0, (int64_t)h->cfg.k * h->batch, count,
+                             h->batch, h->in_dim, h->hidden, h->classes, h->j0, h->mlp_PL, h->mlp_bar,
+                             h->mlp_epoch + 1, h->G, a, true, h->num_sms, s);
   if (e == cudaErrorNotSupported) {
     if (tp) h->tused[SMA_PHASE_REPLICA] -= 2;  // nothing launched: drop the event pair
     *unsupported = true;
@@ -1482,8 +1489,9 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
     return mark_done(h, s);
   }
   if (!fusable && mlp_fused_ok(h)) {
-    // n = 1 MLP round: gradient of every local learner and the fused update of
-    // the replicas and z in ONE kernel (sma_learner_mlp_fused.cu)
+    // n = 1 learner round: gradient of every local learner and the fused update
+    // of the replicas and z in ONE kernel (sma_learner_mlp_fused.cu, or
+    // sma_learner_softmax_fused.cu's cluster for the softmax learner)
     bool unsupported = false;
     STATUS_TRY(fused_mlp_rounds(h, round, 1, (cudaStream_t)stream, &unsupported));
     if (!unsupported) return SMA_OK;

@@ -898,8 +898,9 @@ def test_mlp_cluster_mode_bitwise(torch_cuda, S, orc):
 
 
 def test_learner_steps_softmax_is_per_round(torch_cuda, S, orc):
-    """sma_learner_steps on the softmax learner (no multi-round kernel) equals
-    sma_learner_step per round bitwise, and the oracle within the bar (C1)."""
+    """sma_learner_steps on the softmax learner (the cluster kernel, the rounds
+    of an epoch per launch) equals sma_learner_step per round bitwise, and the
+    oracle within the bar (C1)."""
     torch = torch_cuda
     X, y = sma_inputs.blobs(3_000, seed=4)
     k, b, R = 4, 16, 50
@@ -924,6 +925,77 @@ def test_learner_steps_softmax_is_per_round(torch_cuda, S, orc):
     assert relerr(hs[1].central(), zr) <= TOL
     for h in hs:
         h.close()
+
+
+SOFTMAX_SHAPES = [(784, 10, 16, 4), (784, 10, 5, 3), (784, 10, 16, 8), (784, 10, 16, 1),
+                  (40, 16, 7, 5), (64, 3, 16, 16)]
+
+
+@pytest.mark.parametrize("shape", SOFTMAX_SHAPES, ids=[str(x) for x in SOFTMAX_SHAPES])
+def test_softmax_cluster_rounds(torch_cuda, S, orc, shape):
+    """The softmax learner's cluster kernel (sma_learner_softmax_fused.cu: the
+    gradient and the n = 1 round of all local learners, the rounds of an epoch
+    per launch, the CTAs of one cluster owning feature slices of every replica
+    and of z in shared memory, partial logits exchanged through DSMEM): 60
+    rounds crossing epochs as one sma_learner_steps call and as 60
+    sma_learner_step calls are bitwise equal, and within the bar of the fp64
+    oracle -- as is the per-round kernel path (SMA_LEARNER_FUSE=1).  Shapes
+    (in_dim, classes, b, k): C1, a ragged batch with odd k, 8 learners, one
+    learner, a small in_dim with 16 classes, 16 learners; up to 4 learners the
+    cluster must run, beyond that it runs where its shared memory fits (else the
+    per-round kernels do, and only the oracle bar applies)."""
+    import os
+    torch = torch_cuda
+    in_dim, classes, b, k = shape
+    if in_dim == 784:
+        X, y = sma_inputs.blobs(3_000, seed=4)
+    else:
+        rng = np.random.default_rng(in_dim)
+        X = rng.normal(0, 1, (1_500, in_dim)).astype(np.float32)
+        y = rng.integers(0, classes, 1_500).astype(np.int32)
+    d = classes * (in_dim + 1)
+    R = 60
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    w0 = np.random.default_rng(3).normal(0, 0.01, d).astype(np.float32)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    res, launches = [], []
+    for mode in ("steps", "step", "fuse1"):
+        if mode == "fuse1":
+            os.environ["SMA_LEARNER_FUSE"] = "1"   # read per call
+        try:
+            h = S.Sma(d, k, a, g, m, w0)
+            S.sma_learner_attach(h.h, 0, in_dim, 0, classes, b, Xd, yd, X.shape[0], 99)
+            s = torch.cuda.Stream()
+            l0 = h.launch_count()
+            if mode == "steps":
+                S.sma_learner_steps(h.h, 0, R, s)
+            else:
+                for i in range(R):
+                    S.sma_learner_step(h.h, i, s)
+            s.synchronize()
+            launches.append(h.launch_count() - l0)
+            res.append((h.central(), h.central_prev(), [h.replica(j) for j in range(k)]))
+            h.close()
+        finally:
+            os.environ.pop("SMA_LEARNER_FUSE", None)
+    E = X.shape[0] // (k * b)
+    cluster = launches[1] == R            # one launch per sma_learner_step: the cluster ran
+    if k <= 4:
+        assert cluster, launches
+    assert launches[2] == 2 * R, launches  # the opt-in two-kernel round, for reference
+    if cluster:
+        assert launches[0] == -(-R // E), (launches, E)   # one launch per epoch segment
+    for other in (1,):
+        assert np.array_equal(res[0][0], res[other][0])
+        assert np.array_equal(res[0][1], res[other][1])
+        for j in range(k):
+            assert np.array_equal(res[0][2][j], res[other][2][j]), j
+    zr, zpr, Wr = orc.run_softmax(X, y, b, 99, k, a, g, m, R, w0.astype(np.float64),
+                                  in_dim=in_dim, classes=classes)
+    for z, zp, W in res:
+        assert relerr(z, zr) <= TOL and relerr(zp, zpr) <= TOL
+        for j in range(k):
+            assert relerr(W[j], Wr[j]) <= TOL, j
 
 
 def test_learner_step_fused_matches_unfused(torch_cuda, S, orc):
