@@ -348,6 +348,32 @@ def test_nonfinite_is_reported(torch_cuda, S):
     h.close()
 
 
+@pytest.mark.parametrize("kind", [0, 1])
+def test_nonfinite_is_reported_by_learner_kernels(torch_cuda, S, kind):
+    """SMA_FLAG_CHECK_FINITE on the fused learner rounds (the softmax cluster
+    kernel, the MLP round kernel): an inf in one batch row of the dataset makes
+    the replicas non-finite, the kernel raises the device flag and the next call
+    that reads state reports SMA_ERR_NONFINITE."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(640, seed=4)
+    X = X.copy()
+    X[:, 5] = np.inf                      # every row: whatever the batch draws
+    hidden = 0 if kind == 0 else 32
+    d = 10 * 785 if kind == 0 else hidden * 785 + 10 * hidden + 10
+    h = S.Sma(d, 4, 0.25, 0.1, 0.9, np.full(d, 0.01, np.float32), flags=S.FLAG_CHECK_FINITE)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    S.sma_learner_attach(h.h, kind, 784, hidden, 10, 16, Xd, yd, X.shape[0], 7)
+    s = torch.cuda.Stream()
+    l0 = h.launch_count()
+    S.sma_learner_steps(h.h, 0, 3, s)
+    s.synchronize()
+    assert h.launch_count() - l0 == 1     # one fused launch for the three rounds
+    with pytest.raises(S.SmaError) as e:
+        h.central()
+    assert e.value.status == 4
+    h.close()
+
+
 def test_host_gradient_path_and_timing(torch_cuda, S, orc):
     """sma_set_learner_grads_host (the e2e path) and SMA_FLAG_TIMING."""
     torch = torch_cuda
