@@ -53,6 +53,10 @@
 
 #include <cooperative_groups.h>
 
+#include <array>
+#include <map>
+#include <mutex>
+
 #include "sma_bulk.cuh"
 #include "sma_pdl.cuh"
 #include "sma_internal.h"
@@ -491,27 +495,65 @@ cudaError_t launch_softmax_cluster_rounds(const float* X, const int32_t* y, cons
   if (do_prof && !prof && cudaMalloc(&prof, 16 * 2 * 8 * sizeof(unsigned long long)) != cudaSuccess) return cudaErrorMemoryAllocation;
   auto kfn = do_prof ? softmax_cluster_kernel<true> : softmax_cluster_kernel<false>;
   const void* fn = reinterpret_cast<const void*>(kfn);
-  // slice counts, most parallel first (each slice >= 4 float4s); > 8 needs a
-  // non-portable cluster, which not every GPC may host
-  const int cand[] = {16, 14, 12, 8, 7, 6, 4, 2, 1};
-  for (int M : cand) {
-    if (m_knob > 0 && M != m_knob) continue;
-    if (M > 1 && n4k / M < 4) continue;
-    // row stride in float4s made odd: the 8 rows of one 128-byte wavefront land
-    // on distinct bank groups
-    const int fs4 = (n4k + M - 1) / M;
-    const int fs = 4 * (fs4 | 1);
-    const size_t smem = softmax_smem(a.r, b, classes, fs, M);
-    if (smem > 225 * 1024) continue;
-    cudaError_t e = ensure_dyn_smem(fn, (int)smem);
-    if (e != cudaSuccess) return e;
-    if (M > 8) {
-      e = cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) {
-        cudaGetLastError();
-        continue;
+  // The slice count: the most parallel (each slice >= 4 float4s) whose buffers
+  // fit and whose cluster can be resident (> 8 needs a non-portable cluster,
+  // which not every GPC may host); chosen once per (device, shape) -- the
+  // attribute and occupancy queries cost host microseconds per call.
+  struct Choice { int M, fs; size_t smem; };
+  static std::mutex cache_mu;
+  static std::map<std::array<int, 6>, Choice> cache;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const std::array<int, 6> key = {dev, a.r, b, classes, in_dim, do_prof ? 1 : 0};
+  Choice ch{0, 0, 0};
+  {
+    std::lock_guard<std::mutex> lock(cache_mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+      ch = it->second;
+    } else {
+      const int cand[] = {16, 14, 12, 8, 7, 6, 4, 2, 1};
+      for (int M : cand) {
+        if (m_knob > 0 && M != m_knob) continue;
+        if (M > 1 && n4k / M < 4) continue;
+        // row stride in float4s made odd: the 8 rows of one 128-byte wavefront
+        // land on distinct bank groups
+        const int fs = 4 * (((n4k + M - 1) / M) | 1);
+        const size_t smem = softmax_smem(a.r, b, classes, fs, M);
+        if (smem > 225 * 1024) continue;
+        e = ensure_dyn_smem(fn, (int)smem);
+        if (e != cudaSuccess) return e;
+        if (M > 8 && cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+          cudaGetLastError();
+          continue;
+        }
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3(M);
+        q.blockDim = dim3(kThr);
+        q.dynamicSmemBytes = smem;
+        cudaLaunchAttribute qa;
+        qa.id = cudaLaunchAttributeClusterDimension;
+        qa.val.clusterDim.x = (unsigned)M;
+        qa.val.clusterDim.y = 1;
+        qa.val.clusterDim.z = 1;
+        q.attrs = &qa;
+        q.numAttrs = 1;
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, kfn, &q) != cudaSuccess || nc < 1) {
+          cudaGetLastError();
+          continue;
+        }
+        ch = Choice{M, fs, smem};
+        break;
       }
+      cache[key] = ch;
     }
+  }
+  if (ch.M == 0) return cudaErrorNotSupported;
+  const int M = ch.M, fs = ch.fs;
+  const size_t smem = ch.smem;
+  {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(M);
     cfg.blockDim = dim3(kThr);
@@ -524,11 +566,6 @@ cudaError_t launch_softmax_cluster_rounds(const float* X, const int32_t* y, cons
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    int nc = 0;  // the cluster must be able to be resident at all (M SMs of one GPC)
-    if (cudaOccupancyMaxActiveClusters(&nc, kfn, &cfg) != cudaSuccess || nc < 1) {
-      cudaGetLastError();
-      continue;
-    }
     if (pdl::enabled()) {
       at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
       at[1].val.programmaticStreamSerializationAllowed = 1;
@@ -558,7 +595,6 @@ cudaError_t launch_softmax_cluster_rounds(const float* X, const int32_t* y, cons
     }
     return e;
   }
-  return cudaErrorNotSupported;
 }
 
 }  // namespace sma
