@@ -357,25 +357,33 @@ sma_status sma_learner_attach(sma_handle* h, int32_t kind, int32_t in_dim, int32
  * cuda_stream.  Errors: STATE (no learner attached), CUDA. */
 sma_status sma_learner_grads(sma_handle* h, int64_t round, void* cuda_stream);
 
-/* One full round with the learner in the loop: exactly sma_learner_grads then
- * sma_step (same results).  Under Mode B the z-sync of the round is forked
- * before the learner kernels, so it overlaps them.  With the
- * environment variable SMA_LEARNER_FUSE=1, the softmax learner on a single-GPU
- * handle (no MATERIALIZE_C, no CUDA graph) runs the gradient slice, the replica
- * update and the central update fused in one kernel after the logits kernel
- * (the gradient never makes an HBM round trip; measured slower on B200, so
- * opt-in).  Errors: as sma_learner_grads and sma_step. */
+/* One full round with the learner in the loop: sma_learner_grads then sma_step
+ * (Alg. 1 lines 6-14).  Under Mode B the z-sync of the round is forked before
+ * the learner kernels, so it overlaps them.  On a single-GPU handle
+ * (no MATERIALIZE_C, no CUDA graph) the gradient and the update of every local
+ * learner run as ONE kernel: the MLP round kernel, or the softmax learner's
+ * thread-block cluster (feature slices of every replica and of z in shared
+ * memory, r <= 8, b <= 16, classes <= 16; SMA_SOFTMAX_CLUSTER=0 disables it) --
+ * the same arithmetic per element except the order of the logits' K sum, so
+ * within the oracle bar of the two-call form, not bitwise.  With the
+ * environment variable SMA_LEARNER_FUSE=1 the softmax learner instead runs the
+ * logits kernel then the gradient slice, replica update and central update in
+ * one kernel (bitwise sma_learner_grads + sma_step's ascending-j order).
+ * Errors: as sma_learner_grads and sma_step. */
 sma_status sma_learner_step(sma_handle* h, int64_t round, void* cuda_stream);
 
 /* Rounds round0, round0 + 1, ..., round0 + count - 1 with the learner in the
  * loop: the same results as sma_learner_step called for each of them in turn
- * (bitwise).  For the MLP learner on a single-GPU handle (n = 1, no
- * MATERIALIZE_C, no CUDA graph) the rounds of one epoch (R10) run
- * in ONE launch of the fused kernel: the CTA that owns a learner's block of
- * hidden units keeps that block's weights on chip across the rounds and
- * prefetches the next round's batch rows and z block, and the rounds are
- * ordered by per-CTA flags instead of kernel boundaries; a new epoch starts a
- * new launch.  Every other configuration calls sma_learner_step per round.
+ * (bitwise).  On a single-GPU handle (n = 1, no MATERIALIZE_C, no CUDA graph)
+ * the rounds of one epoch (R10) run in ONE launch of the fused
+ * learner kernel: for the MLP, the CTA that owns a learner's block of hidden
+ * units keeps that block's weights on chip across the rounds and prefetches
+ * the next round's batch rows and z block, the rounds ordered by per-CTA flags
+ * instead of kernel boundaries; for the softmax learner, one thread-block
+ * cluster keeps every replica and z in shared memory for the whole launch and
+ * exchanges partial logits and softmax rows through distributed shared memory.
+ * A new epoch starts a new launch.  Every other configuration calls
+ * sma_learner_step per round.
  * Enqueued on cuda_stream; no host synchronisation.  count = 0 is a no-op.
  * Errors: INVALID_ARG (round0 < 0, count < 0, n_samples < k * batch), STATE
  * (no learner attached), CUDA, and sma_step's. */

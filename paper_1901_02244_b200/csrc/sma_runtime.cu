@@ -1373,7 +1373,7 @@ sma_status sma_learner_grads(sma_handle* h, int64_t round, void* stream) {
 // The n = 1 learner round in one fused kernel applies: the MLP kernel
 // (sma_learner_mlp_fused.cu) or the softmax cluster kernel
 // (sma_learner_softmax_fused.cu).
-static bool mlp_fused_ok(const sma_handle* h) {
+static bool learner_fused_ok(const sma_handle* h) {
   return !h->collective && !h->matc && h->r > 0 && !(h->graphs && !h->timing) &&
          ((h->kind == 1 && mlp_fused_enabled()) || (h->kind == 0 && softmax_cluster_enabled()));
 }
@@ -1382,7 +1382,7 @@ static bool mlp_fused_ok(const sma_handle* h) {
 // in one launch of the fused learner kernel (MLP, or the softmax cluster).
 // *unsupported (nothing enqueued) when
 // the kernel does not cover the shape or count.
-static sma_status fused_mlp_rounds(sma_handle* h, int64_t round0, int count, cudaStream_t s,
+static sma_status fused_learner_rounds(sma_handle* h, int64_t round0, int count, cudaStream_t s,
                                    bool* unsupported) {
   *unsupported = false;
   DeviceGuard guard(h->dev);
@@ -1440,7 +1440,7 @@ sma_status sma_learner_steps(sma_handle* h, int64_t round0, int32_t count, void*
   int64_t i = round0;
   const int64_t end = round0 + count;
   const char* fe = getenv("SMA_LEARNER_FUSE");
-  if (!(fe && fe[0] == '1') && mlp_fused_ok(h)) {
+  if (!(fe && fe[0] == '1') && learner_fused_ok(h)) {
     const int64_t E = h->n_samples / ((int64_t)h->cfg.k * h->batch);
     if (E < 1)
       return fail(SMA_ERR_INVALID_ARG, "n_samples=%lld < k*batch: no full round per epoch",
@@ -1448,7 +1448,7 @@ sma_status sma_learner_steps(sma_handle* h, int64_t round0, int32_t count, void*
     while (i < end) {  // one launch per epoch segment (one permutation per launch)
       const int64_t n = std::min<int64_t>(end - i, E - i % E);
       bool unsupported = false;
-      STATUS_TRY(fused_mlp_rounds(h, i, (int)n, (cudaStream_t)stream, &unsupported));
+      STATUS_TRY(fused_learner_rounds(h, i, (int)n, (cudaStream_t)stream, &unsupported));
       if (unsupported) break;
       i += n;
     }
@@ -1488,12 +1488,12 @@ sma_status sma_learner_step(sma_handle* h, int64_t round, void* stream) {
     advance(h);
     return mark_done(h, s);
   }
-  if (!fusable && mlp_fused_ok(h)) {
+  if (!fusable && learner_fused_ok(h)) {
     // n = 1 learner round: gradient of every local learner and the fused update
     // of the replicas and z in ONE kernel (sma_learner_mlp_fused.cu, or
     // sma_learner_softmax_fused.cu's cluster for the softmax learner)
     bool unsupported = false;
-    STATUS_TRY(fused_mlp_rounds(h, round, 1, (cudaStream_t)stream, &unsupported));
+    STATUS_TRY(fused_learner_rounds(h, round, 1, (cudaStream_t)stream, &unsupported));
     if (!unsupported) return SMA_OK;
   }
   if (!fusable) {  // the same result through the two public calls
