@@ -88,9 +88,11 @@ __device__ __forceinline__ void st_release_gpu(unsigned* p, unsigned v) {
 //       store -- long satisfied by then -- and before it stages z^{i+1});
 //   P2: CTA c has stored its replica block of W^{i+1} (consumers: every CTA,
 //       before its z slice of round i + 1, which reads every replica).
-__device__ __forceinline__ void flag_arrive(unsigned* line, unsigned epoch) {
+// `releaser`: the thread that issues the release store (it waits there for the
+// CTA's outstanding stores), chosen off the next phase's critical path.
+__device__ __forceinline__ void flag_arrive(unsigned* line, unsigned epoch, int releaser = 0) {
   __syncthreads();
-  if (threadIdx.x == 0) st_release_gpu(line, epoch);
+  if ((int)threadIdx.x == releaser) st_release_gpu(line, epoch);
 }
 // Spin until *line >= epoch (acquire).
 __device__ __forceinline__ void flag_poll(const unsigned* line, unsigned epoch) {
@@ -134,6 +136,7 @@ struct MlpRoundArgs {
   int fstride;            // flag lines per kind (>= grid)
   unsigned epoch;         // first round's number (host counter, increasing)
   unsigned long long* prof;  // SMA_MLP_PROF: per-phase cycle sums [grid][16] (or nullptr)
+  int p2rel;              // P2 flag released by group 2 (SMA_MLP_P2REL, default 1)
   ReplicaArgs a;          // W, ld, r, z, zprev_next, alpha, gamma, mu, d, n4, nonfinite
 };
 enum { kFlagPL = 0, kFlagZD = 1, kFlagP2 = 2 };
@@ -879,7 +882,11 @@ __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m
       __syncthreads();   // shared buffers are reused by the next round
       cluster_arrive();  // (P_i) my W^{i+1} (shared memory) is complete for the peers
     } else if (UPDATE && i + 1 < m.count) {
-      flag_arrive(fP2 + 32 * blockIdx.x, ep);
+      // released by the last warp of group 2, whose next duty is to wait for
+      // every CTA's P2 anyway: the release waits ~1.4 us for this CTA's replica
+      // stores, and issued by thread 0 it held up the next round's phase 1
+      // (SMA_MLP_P2REL=0: thread 0, as before)
+      flag_arrive(fP2 + 32 * blockIdx.x, ep, (nzw > 0 && m.p2rel) ? kThr - 32 : 0);
     } else {
       __syncthreads();  // shared buffers are reused by the next round
     }
@@ -1088,6 +1095,11 @@ cudaError_t launch_mlp_round(const float* X, const int32_t* y, const int32_t* pe
   m.PL = PL; m.B2 = PL + 2 * (size_t)num_sms * kRows * 32; m.G = G; m.bar = bar; m.a = a;
   m.fstride = num_sms; m.epoch = epoch;
   m.prof = mlp_prof_buffer();
+  static const int p2rel = [] {
+    const char* e = getenv("SMA_MLP_P2REL");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  m.p2rel = p2rel;
   const int grid = a.r * m.nblk;
   cudaError_t e;
 #define SMA_MLP_ROUND(TU)                                                                      \
