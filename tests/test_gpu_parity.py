@@ -887,6 +887,48 @@ def test_mlp_learner_steps_random_calls_stress(torch_cuda, S, orc, k):
         h.close()
 
 
+@pytest.mark.parametrize("k,b", [(4, 16), (3, 7)])
+def test_softmax_learner_steps_random_calls_stress(torch_cuda, S, orc, k, b):
+    """The softmax cluster kernel: 600 rounds through sma_learner_steps calls of
+    random sizes (1-60 rounds, seeded), back to back on one stream (cluster
+    launches following each other under programmatic dependent launch, crossing
+    epochs), bitwise equal to one sma_learner_step per round; and the oracle's
+    bar on z after the 600 rounds."""
+    torch = torch_cuda
+    X, y = sma_inputs.blobs(2_000, seed=23)
+    R = 600
+    a, g, m = F32(1 / k), F32(0.1), F32(0.9)
+    w0 = np.random.default_rng(9).normal(0, 0.01, 7850).astype(np.float32)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    sizes = []
+    rng = np.random.default_rng(77 + k)
+    while sum(sizes) < R:
+        sizes.append(int(min(rng.integers(1, 61), R - sum(sizes))))
+    hs = []
+    for multi in (False, True):
+        h = S.Sma(7850, k, a, g, m, w0)
+        S.sma_learner_attach(h.h, 0, 784, 0, 10, b, Xd, yd, X.shape[0], 3)
+        s = torch.cuda.Stream()
+        if multi:
+            i = 0
+            for n in sizes:
+                S.sma_learner_steps(h.h, i, n, s)
+                i += n
+        else:
+            for i in range(R):
+                S.sma_learner_step(h.h, i, s)
+        s.synchronize()
+        hs.append(h)
+    assert np.array_equal(hs[0].central(), hs[1].central())
+    assert np.array_equal(hs[0].central_prev(), hs[1].central_prev())
+    for j in range(k):
+        assert np.array_equal(hs[0].replica(j), hs[1].replica(j)), j
+    zr, _, _ = orc.run_softmax(X, y, b, 3, k, a, g, m, R, w0.astype(np.float64))
+    assert relerr(hs[1].central(), zr) <= TOL
+    for h in hs:
+        h.close()
+
+
 def test_mlp_cluster_mode_bitwise(torch_cuda, S, orc):
     """The fused MLP kernel's cluster mode (SMA_MLP_CLUSTER=1: the 4 CTAs of a
     unit block form a thread-block cluster and exchange z^{i+1} through
