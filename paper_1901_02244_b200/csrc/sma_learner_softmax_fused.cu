@@ -20,16 +20,18 @@
 // (8 compute warps; a ninth, producer warp stages the batch-row slices of round
 // i + 1 by TMA and reads the permutation of round i + 2 meanwhile):
 //   P  partial logits of every (learner, row, class) over the CTA's features,
-//      sent into slot q of every CTA's partial buffer with st.async (16-byte
-//      stores into distributed shared memory that count their bytes on the
-//      receiver's mbarrier);
-//   S  once the mbarrier has all m slices' bytes: logits = partials summed in
-//      ascending slice order + bias; e = softmax - onehot (two rows per warp,
-//      the max-subtracted form of sma_softmax.cuh);
-//   G  dW_j[c][slice] = e_j^T X_j / b (ascending t, then / b), db_j (replicated);
-//   U  z^{i+1} = (z^i + sum_j alpha (w_j^i - z^i)) + mu (z^i - z^{i-1}),
-//      corrections in ascending j (R7), into the z^{i-1} half; then
-//      w_j^{i+1} = fma(-gamma, g_j, w_j^i) - alpha (w_j^i - z^i)  (the
+//      sent into slot q of the row's owner (row rr = j b + t, owner rr mod m) with
+//      st.async (16-byte stores into distributed shared memory that count their
+//      bytes on the receiver's mbarrier);
+//   Z  while they fly (no gradient needed): z^{i+1} = (z^i + sum_j c_j) +
+//      mu (z^i - z^{i-1}) with c_j = alpha (w_j^i - z^i) in ascending j (R7),
+//      into the z^{i-1} half, each c_j kept;
+//   S  the owner, once its mbarrier has all m slices' bytes: logits = partials
+//      summed in ascending slice order + bias; e = softmax - onehot (two rows
+//      per warp, the max-subtracted form of sma_softmax.cuh), broadcast to every
+//      CTA the same way;
+//   G  dW_j[c][slice] = e_j^T X_j / b (ascending t, then / b), db_j (replicated),
+//      and right there w_j^{i+1} = fma(-gamma, g_j, w_j^i) - c_j  (the
 //      arithmetic of replica_step_ldg<kFused>).
 // No cluster-wide barrier per round: the partial buffers and their mbarriers
 // alternate by round parity, and a CTA can be at most one round ahead of any
@@ -87,11 +89,6 @@ struct SoftmaxRoundArgs {
   unsigned long long* prof;  // SMA_SOFTMAX_PROF: per-phase cycle sums [grid][2][8] (or nullptr)
 };
 
-// Alg. 1 lines 9-10 with replica_step_ldg<kFused>'s operation order.
-__device__ __forceinline__ float upd(float w, float g, float z, float alpha, float gamma) {
-  const float c = __fmul_rn(alpha, __fsub_rn(w, z));
-  return __fsub_rn(__fmaf_rn(-gamma, g, w), c);
-}
 // DSMEM producer / consumer primitives: st.async writes 16 bytes into a peer's
 // shared memory and counts them on the peer's mbarrier (complete_tx with
 // release semantics at cluster scope); the consumer's wait acquires at cluster
@@ -137,12 +134,13 @@ __global__ void __launch_bounds__(kThr, 1) softmax_cluster_kernel(const SoftmaxR
   const int R = r * b, maxown = (R + M - 1) / M, nown = (R - q + M - 1) / M;
   // shared memory (floats)
   float* ws = sm;                                  // [r][classes][FS] w_j slices
-  float* gs = ws + r * classes * FS;               // [r][classes][FS] gradients
-  float* zs = gs + r * classes * FS;               // [2][classes][FS] z^i / z^{i-1} slices
+  float* gs = ws + r * classes * FS;               // [r][classes][FS] gradients (the last round's)
+  float* cs = gs + r * classes * FS;               // [r][classes][FS] corrections alpha (w_j^i - z^i)
+  float* zs = cs + r * classes * FS;               // [2][classes][FS] z^i / z^{i-1} slices
   float* xs = zs + 2 * classes * FS;               // [2][r][kRows][FS] batch-row slices
   float* pl = xs + 2 * r * kRows * FS;             // [2][M][maxown][kCls] partials of my rows (parity)
   float* es = pl + 2 * M * maxown * kCls;          // [r][kRows][32] softmax - onehot (every row)
-  __shared__ float wb[kMaxR][kCls], gb[kMaxR][kCls], zb[2][kCls];  // biases (replicated)
+  __shared__ float wb[kMaxR][kCls], cb[kMaxR][kCls], gb[kMaxR][kCls], zb[2][kCls];  // biases (replicated)
   __shared__ int rows[3][kMaxR][kRows], ys[2][kMaxR][kRows];
   // [0], [1] batch-row buffers full (TMA bytes + the producer's labels); [2] W
   // and z slices; [3], [4] partial logits of my rows; [5], [6] e rows; [7], [8]
@@ -282,6 +280,51 @@ __global__ void __launch_bounds__(kThr, 1) softmax_cluster_kernel(const SoftmaxR
           st_async4(dst + 16u, make_float4(s[4], s[5], s[6], s[7]), pb);
         }
       }
+      // ---- Z (needs no gradient, so it runs while the partials fly):
+      // z^{i+1} = (z^i + sum_j alpha (w_j^i - z^i)) + mu (z^i - z^{i-1}) from the
+      // pre-update replicas, corrections in ascending j (R7), into the z^{i-1}
+      // half; each c_j = alpha (w_j^i - z^i) kept for the replica update
+      {
+        const float* zc = zs + cur * classes * FS;   // z^i
+        float* zn = zs + (cur ^ 1) * classes * FS;   // z^{i-1} -> z^{i+1}
+        for (int u = tid; u < classes * nf4; u += kProd * 32) {
+          const int c = u / nf4, f = u - c * nf4;
+          const int o = c * FS + 4 * f;
+          const float4 z = *reinterpret_cast<const float4*>(zc + o);
+          const float4 zp = *reinterpret_cast<const float4*>(zn + o);
+          float4 sacc = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int jj = 0; jj < r; ++jj) {
+            const float4 w = *reinterpret_cast<const float4*>(ws + jj * classes * FS + o);
+            float4 cc;
+            cc.x = __fmul_rn(a.alpha, __fsub_rn(w.x, z.x));
+            cc.y = __fmul_rn(a.alpha, __fsub_rn(w.y, z.y));
+            cc.z = __fmul_rn(a.alpha, __fsub_rn(w.z, z.z));
+            cc.w = __fmul_rn(a.alpha, __fsub_rn(w.w, z.w));
+            *reinterpret_cast<float4*>(cs + jj * classes * FS + o) = cc;
+            sacc.x = __fadd_rn(sacc.x, cc.x); sacc.y = __fadd_rn(sacc.y, cc.y);
+            sacc.z = __fadd_rn(sacc.z, cc.z); sacc.w = __fadd_rn(sacc.w, cc.w);
+          }
+          float4 znew;
+          znew.x = __fadd_rn(__fadd_rn(z.x, sacc.x), __fmul_rn(a.mu, __fsub_rn(z.x, zp.x)));
+          znew.y = __fadd_rn(__fadd_rn(z.y, sacc.y), __fmul_rn(a.mu, __fsub_rn(z.y, zp.y)));
+          znew.z = __fadd_rn(__fadd_rn(z.z, sacc.z), __fmul_rn(a.mu, __fsub_rn(z.z, zp.z)));
+          znew.w = __fadd_rn(__fadd_rn(z.w, sacc.w), __fmul_rn(a.mu, __fsub_rn(z.w, zp.w)));
+          *reinterpret_cast<float4*>(zn + o) = znew;
+          bad |= !(isfinite(znew.x) && isfinite(znew.y) && isfinite(znew.z) && isfinite(znew.w));
+        }
+        if (tid < classes) {  // the biases (replicated; every CTA the same bits)
+          const int c = tid;
+          const float z = zb[cur][c];
+          float sacc = 0.f;
+          for (int jj = 0; jj < r; ++jj) {
+            cb[jj][c] = __fmul_rn(a.alpha, __fsub_rn(wb[jj][c], z));
+            sacc = __fadd_rn(sacc, cb[jj][c]);
+          }
+          const float znew = __fadd_rn(__fadd_rn(z, sacc), __fmul_rn(a.mu, __fsub_rn(z, zb[cur ^ 1][c])));
+          zb[cur ^ 1][c] = znew;
+          bad |= !isfinite(znew);
+        }
+      }
       pmark(2);
       // ---- S (my rows): logits = partials in ascending slice order + bias,
       // e = softmax - onehot (two rows per warp, lane = class + 16 * row), sent
@@ -322,7 +365,10 @@ __global__ void __launch_bounds__(kThr, 1) softmax_cluster_kernel(const SoftmaxR
     }
     csync();  // e of every row
 
-    // ---- G: dW_j[c][f] over this slice: item (jj, float4 f, 4 classes)
+    // ---- G: dW_j[c][f] over this slice, item (jj, float4 f, 4 classes), and
+    // right there the replica update w' = fma(-gamma, g, w) - c  (Alg. 1 line 10
+    // with replica_step_ldg<kFused>'s operation order)
+    const bool last = i + 1 == m.count;
     if (!producer) {
       const int nqc = (classes + 3) >> 2;
       for (int it = tid; it < r * nf4 * nqc; it += kProd * 32) {
@@ -352,69 +398,29 @@ __global__ void __launch_bounds__(kThr, 1) softmax_cluster_kernel(const SoftmaxR
               g.x = __fdiv_rn(g.x, fb); g.y = __fdiv_rn(g.y, fb);
               g.z = __fdiv_rn(g.z, fb); g.w = __fdiv_rn(g.w, fb);
             }
-            reinterpret_cast<float4*>(gs + (jj * classes + c0 + u) * FS)[f] = g;
+            const int o = (jj * classes + c0 + u) * FS + 4 * f;
+            if (last) *reinterpret_cast<float4*>(gs + o) = g;
+            float4* wp = reinterpret_cast<float4*>(ws + o);
+            const float4 cc = *reinterpret_cast<const float4*>(cs + o);
+            float4 w = *wp;
+            w.x = __fsub_rn(__fmaf_rn(-a.gamma, g.x, w.x), cc.x);
+            w.y = __fsub_rn(__fmaf_rn(-a.gamma, g.y, w.y), cc.y);
+            w.z = __fsub_rn(__fmaf_rn(-a.gamma, g.z, w.z), cc.z);
+            w.w = __fsub_rn(__fmaf_rn(-a.gamma, g.w, w.w), cc.w);
+            *wp = w;
+            bad |= !(isfinite(w.x) && isfinite(w.y) && isfinite(w.z) && isfinite(w.w));
           }
       }
-      if (tid < r * classes) {  // db (every CTA: replicated)
+      if (tid < r * classes) {  // db and the bias update (every CTA: replicated)
         const int jj = tid / classes, c = tid - jj * classes;
         float s = 0.f;
         for (int t = 0; t < b; ++t) s = __fadd_rn(s, es[(jj * kRows + t) * 32 + c]);
-        gb[jj][c] = pow2 ? __fmul_rn(s, inv_b) : __fdiv_rn(s, fb);
+        const float g = pow2 ? __fmul_rn(s, inv_b) : __fdiv_rn(s, fb);
+        if (last) gb[jj][c] = g;
+        wb[jj][c] = __fsub_rn(__fmaf_rn(-a.gamma, g, wb[jj][c]), cb[jj][c]);
+        bad |= !isfinite(wb[jj][c]);
       }
       pmark(5);
-    }
-    csync();
-
-    // ---- U: z^{i+1} from the pre-update replicas, then the replica update
-    if (!producer) {
-      float* zc = zs + cur * classes * FS;         // z^i
-      float* zn = zs + (cur ^ 1) * classes * FS;   // z^{i-1} -> z^{i+1}
-      for (int u = tid; u < classes * nf4; u += kProd * 32) {
-        const int c = u / nf4, f = u - c * nf4;
-        const int o = c * FS + 4 * f;
-        const float4 z = *reinterpret_cast<const float4*>(zc + o);
-        const float4 zp = *reinterpret_cast<const float4*>(zn + o);
-        float4 sacc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int jj = 0; jj < r; ++jj) {  // corrections in ascending learner (R7)
-          const float4 w = *reinterpret_cast<const float4*>(ws + jj * classes * FS + o);
-          sacc.x = __fadd_rn(sacc.x, __fmul_rn(a.alpha, __fsub_rn(w.x, z.x)));
-          sacc.y = __fadd_rn(sacc.y, __fmul_rn(a.alpha, __fsub_rn(w.y, z.y)));
-          sacc.z = __fadd_rn(sacc.z, __fmul_rn(a.alpha, __fsub_rn(w.z, z.z)));
-          sacc.w = __fadd_rn(sacc.w, __fmul_rn(a.alpha, __fsub_rn(w.w, z.w)));
-        }
-        float4 znew;
-        znew.x = __fadd_rn(__fadd_rn(z.x, sacc.x), __fmul_rn(a.mu, __fsub_rn(z.x, zp.x)));
-        znew.y = __fadd_rn(__fadd_rn(z.y, sacc.y), __fmul_rn(a.mu, __fsub_rn(z.y, zp.y)));
-        znew.z = __fadd_rn(__fadd_rn(z.z, sacc.z), __fmul_rn(a.mu, __fsub_rn(z.z, zp.z)));
-        znew.w = __fadd_rn(__fadd_rn(z.w, sacc.w), __fmul_rn(a.mu, __fsub_rn(z.w, zp.w)));
-        *reinterpret_cast<float4*>(zn + o) = znew;
-        bad |= !(isfinite(znew.x) && isfinite(znew.y) && isfinite(znew.z) && isfinite(znew.w));
-        for (int jj = 0; jj < r; ++jj) {
-          float4* wp = reinterpret_cast<float4*>(ws + jj * classes * FS + o);
-          const float4 g = *reinterpret_cast<const float4*>(gs + jj * classes * FS + o);
-          float4 w = *wp;
-          w.x = upd(w.x, g.x, z.x, a.alpha, a.gamma);
-          w.y = upd(w.y, g.y, z.y, a.alpha, a.gamma);
-          w.z = upd(w.z, g.z, z.z, a.alpha, a.gamma);
-          w.w = upd(w.w, g.w, z.w, a.alpha, a.gamma);
-          *wp = w;
-          bad |= !(isfinite(w.x) && isfinite(w.y) && isfinite(w.z) && isfinite(w.w));
-        }
-      }
-      if (tid < classes) {  // the biases (replicated; every CTA the same bits)
-        const int c = tid;
-        const float z = zb[cur][c];
-        float sacc = 0.f;
-        for (int jj = 0; jj < r; ++jj) sacc = __fadd_rn(sacc, __fmul_rn(a.alpha, __fsub_rn(wb[jj][c], z)));
-        const float znew = __fadd_rn(__fadd_rn(z, sacc), __fmul_rn(a.mu, __fsub_rn(z, zb[cur ^ 1][c])));
-        zb[cur ^ 1][c] = znew;
-        bad |= !isfinite(znew);
-        for (int jj = 0; jj < r; ++jj) {
-          wb[jj][c] = upd(wb[jj][c], gb[jj][c], z, a.alpha, a.gamma);
-          bad |= !isfinite(wb[jj][c]);
-        }
-      }
-      pmark(6);
     }
     csync();  // w^{i+1}, z^{i+1} complete (the next round's partial logits)
     if (tid == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&mbar[7 + cur])) : "memory");
@@ -458,7 +464,7 @@ __global__ void __launch_bounds__(kThr, 1) softmax_cluster_kernel(const SoftmaxR
 
 size_t softmax_smem(int r, int b, int classes, int fs, int M) {
   const size_t npl = (size_t)((r * b + M - 1) / M) * kCls;
-  return sizeof(float) * (2 * (size_t)r * classes * fs + 2 * (size_t)classes * fs + 2 * (size_t)r * kRows * fs +
+  return sizeof(float) * (3 * (size_t)r * classes * fs + 2 * (size_t)classes * fs + 2 * (size_t)r * kRows * fs +
                           2 * (size_t)M * npl + (size_t)r * kRows * 32);
 }
 }  // namespace
@@ -582,7 +588,7 @@ cudaError_t launch_softmax_cluster_rounds(const float* X, const int32_t* y, cons
       cudaMemcpy(h, prof, sizeof(unsigned long long) * M * 16, cudaMemcpyDeviceToHost);
       int khz = 0;
       cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, 0);
-      const char* nm[7] = {"producer", "rows_wait", "partials+send", "my_rows_softmax", "e_wait", "dW", "update"};
+      const char* nm[7] = {"producer", "rows_wait", "partials+send+z", "my_rows_softmax", "e_wait", "dW+update", "-"};
       for (int w = 0; w < 2; ++w) {
         fprintf(stderr, "SMA_SOFTMAX_PROF M=%d r=%d count=%d thread %d:", M, a.r, count, w * kProd * 32);
         for (int ph = 0; ph < 7; ++ph) {
