@@ -1,0 +1,8 @@
+# round 2, call MU: fused MLP kernel, dW1 row loop unrolled by 4 -- multi-round rates k = 4 / 8 / 16, profile k = 4
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+S=gpurun_out/status_mu.txt; : > $S
+for k in 4 8 16; do
+  timeout 300 python bench.py --config MLP --k $k --steps 3000 --warmup 50 --rounds-per-call 3000 --no-cpu-baseline --no-e2e > gpurun_out/mu_k$k.log 2>&1; echo k$k=$? >> $S
+done
+SMA_MLP_PROF=3 timeout 300 python bench.py --config MLP --k 4 --steps 1000 --warmup 20 --rounds-per-call 1000 --no-cpu-baseline --no-e2e > gpurun_out/mu_prof.log 2>&1
+echo done >> $S
