@@ -188,6 +188,10 @@ __global__ void __launch_bounds__(kThr, 1) softmax_cluster_kernel(const SoftmaxR
   for (int u = tid; u < 2 * r * kRows * FS; u += kThr) xs[u] = 0.f;  // rows t >= b stay 0
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");        // before the TMA writes
   __syncthreads();
+  // split cluster barrier: arrive now (the mbarrier inits are fenced at cluster
+  // scope), wait only right before this CTA's first st.async into a peer -- the
+  // launch's staging overlaps the other CTAs' start
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
   if (producer) {
     load_rows(0);
     if (m.count > 1) load_rows(1);
@@ -214,7 +218,9 @@ __global__ void __launch_bounds__(kThr, 1) softmax_cluster_kernel(const SoftmaxR
   }
   bulk::wait(&mbar[2], 0);
   __syncthreads();
-  clu.sync();  // every CTA of the cluster is running, its mbarriers initialised
+  // every CTA of the cluster is running and its mbarriers exist (the compute
+  // warps send partial logits into them from round 0 on)
+  asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
 
   bool bad = false;
   unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
