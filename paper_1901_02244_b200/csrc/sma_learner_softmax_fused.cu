@@ -118,13 +118,15 @@ __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
 
 // SMA_SOFTMAX_PROF (debugging only): threads 0 and kProd * 32 (the producer)
 // accumulate clock64() cycles per phase over the launch's rounds.
-template <bool PROF>
+// FB: the batch size as a compile-time constant (16, the paper's b for C1: the
+// per-row loops unroll fully) or 0 (read from the arguments).
+template <bool PROF, int FB>
 __global__ void __launch_bounds__(kThr, 1) softmax_cluster_kernel(const SoftmaxRoundArgs m) {
   extern __shared__ __align__(16) float sm[];
   const cg::cluster_group clu = cg::this_cluster();
   const int q = (int)clu.block_rank();  // feature slice
   const ReplicaArgs& a = m.a;
-  const int r = a.r, M = m.m, in_dim = m.in_dim, classes = m.classes, b = m.b, FS = m.fs;
+  const int r = a.r, M = m.m, in_dim = m.in_dim, classes = m.classes, b = FB ? FB : m.b, FS = m.fs;
   const int n4k = in_dim >> 2;
   const int f4lo = q * n4k / M, f4hi = (q + 1) * n4k / M, nf4 = f4hi - f4lo;  // this slice
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -370,6 +372,7 @@ __global__ void __launch_bounds__(kThr, 1) softmax_cluster_kernel(const SoftmaxR
       pmark(4);
     }
     csync();  // e of every row
+    if (!producer) pmark(6);
 
     // ---- G: dW_j[c][f] over this slice, item (jj, float4 f, 4 classes), and
     // right there the replica update w' = fma(-gamma, g, w) - c  (Alg. 1 line 10
@@ -505,7 +508,8 @@ cudaError_t launch_softmax_cluster_rounds(const float* X, const int32_t* y, cons
   static unsigned long long* prof = nullptr;
   const bool do_prof = prof_n > 0 && ++nlaunch == prof_n;
   if (do_prof && !prof && cudaMalloc(&prof, 16 * 2 * 8 * sizeof(unsigned long long)) != cudaSuccess) return cudaErrorMemoryAllocation;
-  auto kfn = do_prof ? softmax_cluster_kernel<true> : softmax_cluster_kernel<false>;
+  auto kfn = b == kRows ? (do_prof ? softmax_cluster_kernel<true, kRows> : softmax_cluster_kernel<false, kRows>)
+                        : (do_prof ? softmax_cluster_kernel<true, 0> : softmax_cluster_kernel<false, 0>);
   const void* fn = reinterpret_cast<const void*>(kfn);
   // The slice count: the most parallel (each slice >= 4 float4s) whose buffers
   // fit and whose cluster can be resident (> 8 needs a non-portable cluster,
@@ -517,7 +521,7 @@ cudaError_t launch_softmax_cluster_rounds(const float* X, const int32_t* y, cons
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  const std::array<int, 6> key = {dev, a.r, b, classes, in_dim, do_prof ? 1 : 0};
+  const std::array<int, 6> key = {dev, a.r, b, classes, in_dim, do_prof ? 1 : 0};  // (b picks the instantiation)
   Choice ch{0, 0, 0};
   {
     std::lock_guard<std::mutex> lock(cache_mu);
@@ -594,7 +598,7 @@ cudaError_t launch_softmax_cluster_rounds(const float* X, const int32_t* y, cons
       cudaMemcpy(h, prof, sizeof(unsigned long long) * M * 16, cudaMemcpyDeviceToHost);
       int khz = 0;
       cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, 0);
-      const char* nm[7] = {"producer", "rows_wait", "partials+send+z", "my_rows_softmax", "e_wait", "dW+update", "-"};
+      const char* nm[7] = {"producer", "rows_wait", "partials+send+z", "my_rows_softmax", "e_wait", "dW+update", "csync_e(before dW)"};
       for (int w = 0; w < 2; ++w) {
         fprintf(stderr, "SMA_SOFTMAX_PROF M=%d r=%d count=%d thread %d:", M, a.r, count, w * kProd * 32);
         for (int ph = 0; ph < 7; ++ph) {
