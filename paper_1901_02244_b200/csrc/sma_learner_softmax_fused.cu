@@ -118,15 +118,16 @@ __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
 
 // SMA_SOFTMAX_PROF (debugging only): threads 0 and kProd * 32 (the producer)
 // accumulate clock64() cycles per phase over the launch's rounds.
-// FB: the batch size as a compile-time constant (16, the paper's b for C1: the
-// per-row loops unroll fully) or 0 (read from the arguments).
-template <bool PROF, int FB>
+// FB, FC: the batch size and the class count as compile-time constants (16 and
+// 10: config C1 -- the per-row and per-class loops unroll fully, the class
+// guards fold) or 0 (read from the arguments).
+template <bool PROF, int FB, int FC>
 __global__ void __launch_bounds__(kThr, 1) softmax_cluster_kernel(const SoftmaxRoundArgs m) {
   extern __shared__ __align__(16) float sm[];
   const cg::cluster_group clu = cg::this_cluster();
   const int q = (int)clu.block_rank();  // feature slice
   const ReplicaArgs& a = m.a;
-  const int r = a.r, M = m.m, in_dim = m.in_dim, classes = m.classes, b = FB ? FB : m.b, FS = m.fs;
+  const int r = a.r, M = m.m, in_dim = m.in_dim, classes = FC ? FC : m.classes, b = FB ? FB : m.b, FS = m.fs;
   const int n4k = in_dim >> 2;
   const int f4lo = q * n4k / M, f4hi = (q + 1) * n4k / M, nf4 = f4hi - f4lo;  // this slice
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -508,8 +509,9 @@ cudaError_t launch_softmax_cluster_rounds(const float* X, const int32_t* y, cons
   static unsigned long long* prof = nullptr;
   const bool do_prof = prof_n > 0 && ++nlaunch == prof_n;
   if (do_prof && !prof && cudaMalloc(&prof, 16 * 2 * 8 * sizeof(unsigned long long)) != cudaSuccess) return cudaErrorMemoryAllocation;
-  auto kfn = b == kRows ? (do_prof ? softmax_cluster_kernel<true, kRows> : softmax_cluster_kernel<false, kRows>)
-                        : (do_prof ? softmax_cluster_kernel<true, 0> : softmax_cluster_kernel<false, 0>);
+  const bool c1 = b == kRows && classes == 10;
+  auto kfn = c1 ? (do_prof ? softmax_cluster_kernel<true, kRows, 10> : softmax_cluster_kernel<false, kRows, 10>)
+                : (do_prof ? softmax_cluster_kernel<true, 0, 0> : softmax_cluster_kernel<false, 0, 0>);
   const void* fn = reinterpret_cast<const void*>(kfn);
   // The slice count: the most parallel (each slice >= 4 float4s) whose buffers
   // fit and whose cluster can be resident (> 8 needs a non-portable cluster,
