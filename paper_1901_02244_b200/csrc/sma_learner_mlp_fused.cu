@@ -198,13 +198,14 @@ __device__ __forceinline__ void fence_proxy_async() {
 // b1, W2 columns; b2 to block 0), so the updates touch disjoint data.
 // The arithmetic per element is replica_step_ldg<kFused>'s, so a round is
 // bitwise the same as gradients-then-update with these gradients.
-// FB: the batch size as a compile-time constant (16, the bench's b: the per-row
-// loops unroll fully) or 0 (read from the arguments).
-template <int TU, bool UPDATE, bool PROF, int FB>
+// FB, FC: the batch size and the class count as compile-time constants (16 and
+// 10, the bench's shape: the per-row and per-class loops unroll fully) or 0
+// (read from the arguments).
+template <int TU, bool UPDATE, bool PROF, int FB, int FC>
 __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m) {
   constexpr int CU = TU * kUG;  // units per phase-1 chunk (<= 32)
   extern __shared__ __align__(16) float sm[];
-  const int in_dim = m.in_dim, hidden = m.hidden, classes = m.classes, b = FB ? FB : m.b, U = m.U;
+  const int in_dim = m.in_dim, hidden = m.hidden, classes = FC ? FC : m.classes, b = FB ? FB : m.b, U = m.U;
   const int nch = m.nch, nblk = m.nblk;
   // rows padded to xld = in_dim + 4 floats: consecutive rows then start 20
   // banks apart (784 + 4 = 788 = 20 mod 32), so the 8 batch-row groups and the
@@ -937,10 +938,13 @@ int mlp_zwarps(int count, bool cl = false) {
 
 template <int TU, bool UPDATE>
 cudaError_t launch_tu(const MlpRoundArgs& m, int grid, size_t smem, cudaStream_t s) {
-  // b = 16 unrolled where it fits the register budget (TU = 1 spills with it)
+  // b = 16 and classes = 10 unrolled where it fits the register budget (TU = 1
+  // spills with it); other shapes use the generic instantiation
   constexpr int kFB = TU >= 2 ? kRows : 0;
-  auto k = m.b == kRows ? (m.prof ? mlp_round_kernel<TU, UPDATE, true, kFB> : mlp_round_kernel<TU, UPDATE, false, kFB>)
-                        : (m.prof ? mlp_round_kernel<TU, UPDATE, true, 0> : mlp_round_kernel<TU, UPDATE, false, 0>);
+  constexpr int kFC = TU >= 2 ? 10 : 0;
+  const bool fixed = m.b == kRows && m.classes == 10;
+  auto k = fixed ? (m.prof ? mlp_round_kernel<TU, UPDATE, true, kFB, kFC> : mlp_round_kernel<TU, UPDATE, false, kFB, kFC>)
+                 : (m.prof ? mlp_round_kernel<TU, UPDATE, true, 0, 0> : mlp_round_kernel<TU, UPDATE, false, 0, 0>);
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(k), (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
