@@ -201,11 +201,12 @@ __device__ __forceinline__ void fence_proxy_async() {
 // FB, FC: the batch size and the class count as compile-time constants (16 and
 // 10, the bench's shape: the per-row and per-class loops unroll fully) or 0
 // (read from the arguments).
-template <int TU, bool UPDATE, bool PROF, int FB, int FC>
+template <int TU, bool UPDATE, bool PROF, int FB, int FC, int FI = 0>
 __global__ void __launch_bounds__(kThr, 2) mlp_round_kernel(const MlpRoundArgs m) {
   constexpr int CU = TU * kUG;  // units per phase-1 chunk (<= 32)
   extern __shared__ __align__(16) float sm[];
-  const int in_dim = m.in_dim, hidden = m.hidden, classes = FC ? FC : m.classes, b = FB ? FB : m.b, U = m.U;
+  const int in_dim = FI ? FI : m.in_dim, hidden = m.hidden, classes = FC ? FC : m.classes, b = FB ? FB : m.b,
+            U = m.U;
   const int nch = m.nch, nblk = m.nblk;
   // rows padded to xld = in_dim + 4 floats: consecutive rows then start 20
   // banks apart (784 + 4 = 788 = 20 mod 32), so the 8 batch-row groups and the
@@ -942,8 +943,10 @@ cudaError_t launch_tu(const MlpRoundArgs& m, int grid, size_t smem, cudaStream_t
   // spills with it); other shapes use the generic instantiation
   constexpr int kFB = TU >= 2 ? kRows : 0;
   constexpr int kFC = TU >= 2 ? 10 : 0;
-  const bool fixed = m.b == kRows && m.classes == 10;
-  auto k = fixed ? (m.prof ? mlp_round_kernel<TU, UPDATE, true, kFB, kFC> : mlp_round_kernel<TU, UPDATE, false, kFB, kFC>)
+  constexpr int kFI = TU >= 2 ? 784 : 0;
+  const bool fixed = m.b == kRows && m.classes == 10 && m.in_dim == 784;
+  auto k = fixed ? (m.prof ? mlp_round_kernel<TU, UPDATE, true, kFB, kFC, kFI>
+                           : mlp_round_kernel<TU, UPDATE, false, kFB, kFC, kFI>)
                  : (m.prof ? mlp_round_kernel<TU, UPDATE, true, 0, 0> : mlp_round_kernel<TU, UPDATE, false, 0, 0>);
   cudaError_t e = ensure_dyn_smem(reinterpret_cast<const void*>(k), (int)smem);
   if (e != cudaSuccess) return e;
